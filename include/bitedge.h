@@ -1,0 +1,148 @@
+/* bitedge.h -- C ABI of the B200 (sm_100a) method-of-masks edge detector.
+ *
+ * The reference (`bitedge`, /root/reference/pkg) is pure Python/numpy and has
+ * no FFI; this ABI is the boundary its Python API binds to (ctypes, see
+ * paper_1401_5245_b200/_capi.py and INTEGRATION.md).  Each entry point names
+ * the reference operation it replaces.
+ *
+ * Raster layout (bitimage.py:1-11): one pixel per bit, 1 = white, 0 = black,
+ * rows packed MSB-first (the MSB of a word is its leftmost pixel).  Two word
+ * formats are accepted, selected by `word_bits`:
+ *   64 -- native uint64 words, the reference's BitImage.words layout
+ *         (bitimage.py:91-97); shape [n, h, row_stride] with
+ *         row_stride >= ceil(w/64);
+ *   32 -- uint32 row words, BASELINE.json's pre-packed format (configs 3, 4);
+ *         row_stride >= ceil(w/32).
+ * `row_stride_words` counts words of the selected format.  Images of a batch
+ * are contiguous ([n][h][row_stride]).  Input padding bits (pixels >= w) may
+ * hold anything and are never read for a visible output; every packed output
+ * has its padding bits set to 1, as the reference's constructor forces
+ * (bitimage.py:101-104).
+ *
+ * Border policy (bitimage.py:56-64): fill_bit 1 = WHITE_OUTSIDE (the default
+ * of every reference entry point), 0 = BLACK_OUTSIDE.
+ *
+ * Conventions: the caller owns every buffer (device pointers unless stated);
+ * nothing is allocated; every launch is asynchronous on `stream` (a
+ * cudaStream_t, NULL = legacy default stream).  Return 0 on success, a
+ * negative BE_E* code for invalid arguments (message in be_last_error(),
+ * mapped to ValueError by the Python layer), or a positive cudaError_t.  The
+ * library keeps no global mutable state besides a thread-local error string,
+ * so it is reentrant; outputs never alias inputs unless stated.
+ */
+#ifndef BITEDGE_H
+#define BITEDGE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BE_ABI_VERSION 1
+
+enum {
+    BE_OK = 0,
+    BE_EINVAL = -1,     /* bad size / stride / pointer / enum */
+    BE_EALIGN = -2,     /* misaligned pointer for the requested format */
+    BE_ESHAPE = -3      /* operand dimensions disagree */
+};
+
+/* Direction enum, (dx, dy) with y growing downwards (bitimage.py:35-41). */
+enum { BE_LEFT = 0, BE_RIGHT = 1, BE_UP = 2, BE_DOWN = 3 };
+
+/* Binary/unary word ops (bitimage.py:181-205). */
+enum { BE_OP_NOT = 0, BE_OP_AND = 1, BE_OP_OR = 2 };
+
+/* Optional outputs of the fused edge kernel; any pointer may be NULL.
+ *   edges    detect_edges_mask: NOT(OR of the four fundamental edges),
+ *            edges black (0) on white
+ *   edgeset  the pre-inversion OR, 1 = edge pixel
+ *   side[s]  fundamental_edge(img, build_mask(img), s) for s = BE_LEFT..BE_DOWN,
+ *            i.e. shift(img, opposite(s)) AND NOT img
+ *   packed   the packed input itself (from_array, bitimage.py:122-136); only
+ *            meaningful for the uint8 entry points
+ * All outputs share word format and row stride. */
+typedef struct be_outputs {
+    void *edges;
+    void *edgeset;
+    void *side[4];
+    void *packed;
+} be_outputs;
+
+/* ---- the fused hot path ------------------------------------------------- */
+
+/* K1. detect_edges_mask on packed rasters (SPEC.md:165-168 composed from
+ * bitimage.py:181-240): out = C | ~(Ln | Rn | Un | Dn), padding = 1.
+ * emit_edgeset != 0 writes the EdgeSet instead. */
+int be_edge_packed_u32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream);
+int be_edge_packed_u64(const uint64_t *in, uint64_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream);
+
+/* K2. BitImage.from_array (bitimage.py:122-136: nonzero byte -> white) fused
+ * with K1.  `in` is uint8 [n, h, in_row_stride bytes]; `out` uint32 words with
+ * out_row_stride_words; packed_in_or_null additionally receives the packed
+ * input (same stride). */
+int be_pack_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int fill_bit,
+                    uint32_t *packed_in_or_null, void *stream);
+
+/* K3. K1 on a row slab of one image whose row -1 / row `rows` come from
+ * neighbour slabs (the received halo rows) instead of the border fill; only
+ * output rows [row_lo, row_hi) are written.  A NULL halo means the slab touches
+ * the image border there and the fill applies (bitimage.py:216-223). */
+int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
+                            const uint32_t *below_or_null, uint32_t *out, int64_t rows, int64_t w,
+                            int64_t row_stride_words, int fill_bit, int64_t row_lo, int64_t row_hi,
+                            void *stream);
+
+/* General form of K1/K2/K3 with every optional output (F3 of SURVEY 8(f)).
+ * input_kind 0: packed words of `word_bits`; 1: uint8 pixels (in_row_stride
+ * in bytes).  above/below as in K3 (n must be 1 when either is non-NULL). */
+int be_edges_general(const void *in, int input_kind, int64_t in_row_stride,
+                     const void *above_or_null, const void *below_or_null,
+                     const be_outputs *outs, int word_bits, int64_t out_row_stride_words,
+                     int64_t n, int64_t h, int64_t w, int fill_bit, int64_t row_lo,
+                     int64_t row_hi, void *stream);
+
+/* ---- BitImage primitives (bitimage.py), device-resident ------------------ */
+
+/* from_array (bitimage.py:122-136): uint8 -> packed, nonzero = white, pad = 1. */
+int be_pack_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+               int64_t in_row_stride, int64_t out_row_stride_words, void *stream);
+/* to_array (bitimage.py:149-153): packed -> uint8 {0,1}. */
+int be_unpack_u8(const void *in, uint8_t *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                 int64_t in_row_stride_words, int64_t out_row_stride, void *stream);
+/* invert / & / | (bitimage.py:181-205); b unused for NOT; padding = 1. */
+int be_bitop(int op, const void *a, const void *b, void *out, int word_bits, int64_t n,
+             int64_t h, int64_t w, int64_t row_stride_words, void *stream);
+/* shift (bitimage.py:207-240): out(x, y) = in(x - dx, y - dy), outside = fill. */
+int be_shift(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+             int64_t row_stride_words, int direction, int fill_bit, void *stream);
+/* fundamental_edge with an explicit mask:
+ * out = shift(img, opposite(side), fill) AND mask, fused in one pass. */
+int be_shift_and(const void *img, const void *mask, void *out, int word_bits, int64_t n,
+                 int64_t h, int64_t w, int64_t row_stride_words, int side, int fill_bit,
+                 void *stream);
+/* count_black (bitimage.py:244-249) per image into counts[n] (int64, device). */
+int be_count_black(const void *in, int64_t *counts, int word_bits, int64_t n, int64_t h,
+                   int64_t w, int64_t row_stride_words, void *stream);
+
+/* detect_edges_scan: the paper's per-pixel Edge(p) scanner
+ * on the device, bit by bit -- an algorithm independent of K1, exposed for the
+ * reference API and as a full-size cross-check. */
+int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                  int64_t row_stride_words, int fill_bit, void *stream);
+
+/* ---- misc ----------------------------------------------------------------- */
+const char *be_last_error(void);
+int be_abi_version(void);
+/* Number of kernels this thread has launched through the ABI (for bench.py's
+ * gpu_launches accounting). */
+int64_t be_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITEDGE_H */

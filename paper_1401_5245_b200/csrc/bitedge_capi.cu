@@ -1,0 +1,529 @@
+// bitedge_capi.cu -- C ABI (include/bitedge.h) over the sm_100a kernels.
+//
+// Host side: argument validation with the reference's error semantics
+// (bitimage.py:87-97, 188-193), tile-shape selection for the fused edge
+// kernel (edge_tile.cuh), and the small word-parallel kernels behind the
+// BitImage primitives (bitimage.py:149-249).  No allocation, no global state
+// beyond thread-local error text and launch counter.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "../../include/bitedge.h"
+#include "edge_tile.cuh"
+
+using namespace bitedge;
+
+namespace {
+
+thread_local char g_err[512];
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_check(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+        return (int)e;
+    }
+    ++g_launches;
+    return BE_OK;
+}
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct Geometry {
+    int64_t n, h, w;
+    int word_bits;
+    int wp;          // storage words per row in uint32 units
+    int pl;
+    uint32_t lastbit, padmask, fillword;
+    int swap;
+};
+
+int make_geometry(Geometry &G, int word_bits, int64_t n, int64_t h, int64_t w, int fill_bit) {
+    if (word_bits != 32 && word_bits != 64)
+        return fail(BE_EINVAL, "word_bits must be 32 or 64, got %d", word_bits);
+    if (n < 0) return fail(BE_EINVAL, "batch size must be >= 0, got %lld", (long long)n);
+    if (w < 1 || h < 1)
+        return fail(BE_EINVAL, "image dimensions must be at least 1x1, got %lldx%lld",
+                    (long long)w, (long long)h);
+    if (fill_bit != 0 && fill_bit != 1)
+        return fail(BE_EINVAL, "fill_bit must be 0 or 1, got %d", fill_bit);
+    if (w > (int64_t)1 << 36 || n * h > ((int64_t)1 << 40))
+        return fail(BE_EINVAL, "raster too large");
+    G.n = n; G.h = h; G.w = w; G.word_bits = word_bits;
+    const int64_t wp = word_bits == 64 ? 2 * ((w + 63) / 64) : (w + 31) / 32;
+    if (wp > (1 << 30)) return fail(BE_EINVAL, "row too wide");
+    G.wp = (int)wp;
+    G.pl = (int)((w - 1) / 32);
+    G.lastbit = 1u << (31 - (int)((w - 1) % 32));
+    G.padmask = G.lastbit - 1u;
+    G.fillword = fill_bit ? 0xFFFFFFFFu : 0u;
+    G.swap = word_bits == 64 ? 1 : 0;
+    return BE_OK;
+}
+
+int check_stride(const Geometry &G, int64_t stride_words, const char *what) {
+    const int64_t need = G.word_bits == 64 ? (G.w + 63) / 64 : (G.w + 31) / 32;
+    if (stride_words < need)
+        return fail(BE_EINVAL, "%s row stride %lld words < %lld words per row", what,
+                    (long long)stride_words, (long long)need);
+    return BE_OK;
+}
+
+int check_ptr(const void *p, int word_bits, const char *what) {
+    if (p == nullptr) return fail(BE_EINVAL, "%s is NULL", what);
+    if (((uintptr_t)p) % (word_bits / 8) != 0)
+        return fail(BE_EALIGN, "%s is not %d-byte aligned", what, word_bits / 8);
+    return BE_OK;
+}
+
+inline int ilog2(int v) { int l = 0; while ((1 << (l + 1)) <= v) ++l; return l; }
+inline int next_pow2(int64_t v) { int p = 1; while (p < v && p < (1 << 30)) p <<= 1; return p; }
+
+template <int KIND>
+int launch_tile(TileParams &tp, int64_t rows, cudaStream_t st) {
+    const int TQ = 1 << tp.log_tq, R = 1 << tp.log_r;
+    const size_t smem = (size_t)(R + 2) * (TQ + 8) * 4 + R;
+    const int64_t tiles_y = (rows + R - 1) / R;
+    const int64_t grid = tiles_y * tp.tiles_x;
+    if (grid <= 0) return BE_OK;
+    if (grid > 0x7FFFFFFFLL) return fail(BE_EINVAL, "raster too large for one launch");
+    edge_tile_kernel<KIND><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    return cuda_check("edge_tile_kernel");
+}
+
+// Shared driver of every fused-edge entry point.
+int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *above,
+               const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
+               uint32_t *o_packed, int word_bits, int64_t out_stride_words, int64_t n, int64_t h,
+               int64_t w, int fill_bit, int64_t row_lo, int64_t row_hi, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, fill_bit);
+    if (rc) return rc;
+    if (n == 0) return BE_OK;
+    if (in == nullptr) return fail(BE_EINVAL, "input is NULL");
+    if (input_kind != 0 && input_kind != 1)
+        return fail(BE_EINVAL, "input_kind must be 0 (packed) or 1 (uint8)");
+    if ((rc = check_stride(G, out_stride_words, "output"))) return rc;
+    uint32_t *outs[7] = {o_edges, o_eset, o_side[0], o_side[1], o_side[2], o_side[3], o_packed};
+    int any = 0;
+    for (int i = 0; i < 7; ++i) {
+        if (outs[i] == nullptr) continue;
+        any = 1;
+        if ((rc = check_ptr(outs[i], word_bits, "output"))) return rc;
+        if ((const void *)outs[i] == in) return fail(BE_EINVAL, "output aliases the input");
+    }
+    if (!any) return fail(BE_EINVAL, "no output requested");
+    if ((above || below) && n != 1)
+        return fail(BE_EINVAL, "halo rows require a single slab (n == 1)");
+    const int64_t nrows = n * h;
+    if (row_lo < 0 || row_hi > nrows || row_lo > row_hi)
+        return fail(BE_EINVAL, "row range [%lld, %lld) outside [0, %lld)", (long long)row_lo,
+                    (long long)row_hi, (long long)nrows);
+    if (row_lo == row_hi) return BE_OK;
+
+    TileParams tp;
+    memset(&tp, 0, sizeof(tp));
+    tp.in = in; tp.above = above; tp.below = below;
+    tp.o_edges = o_edges; tp.o_eset = o_eset;
+    for (int s = 0; s < 4; ++s) tp.o_side[s] = o_side[s];
+    tp.o_packed = o_packed;
+    // strides in uint32 units for packed data
+    tp.out_stride = word_bits == 64 ? 2 * out_stride_words : out_stride_words;
+    tp.nrows = nrows; tp.h = h; tp.w = w; tp.row_lo = row_lo; tp.row_hi = row_hi;
+    tp.wp = G.wp; tp.pl = G.pl; tp.lastbit = G.lastbit; tp.padmask = G.padmask;
+    tp.fillword = G.fillword; tp.swap = G.swap;
+
+    // tile shape: TQ pixel words (power of two <= 64) x R rows, ~16 KB of
+    // packed input or ~32 KB of uint8 input per CTA, smem <= 48 KB.
+    const int TQ = G.wp <= 64 ? next_pow2(G.wp) : 64;
+    const int64_t words_per_tile = input_kind == 1 ? 1024 : 4096;
+    int64_t R = words_per_tile / TQ;
+    const int64_t smem_cap_rows = (48 * 1024) / ((TQ + 8) * 4 + 1) - 2;
+    while (R > smem_cap_rows) R >>= 1;
+    const int64_t rows = row_hi - row_lo;
+    while (R > 1 && R / 2 >= rows) R >>= 1;
+    if (R < 1) R = 1;
+    tp.log_tq = ilog2(TQ);
+    tp.log_r = ilog2((int)R);
+    tp.tiles_x = (G.wp + TQ - 1) / TQ;
+
+    cudaStream_t st = S(stream);
+    if (input_kind == 0) {
+        if ((rc = check_ptr(in, word_bits, "input"))) return rc;
+        if ((rc = check_stride(G, in_stride, "input"))) return rc;
+        if (above && (rc = check_ptr(above, word_bits, "above halo"))) return rc;
+        if (below && (rc = check_ptr(below, word_bits, "below halo"))) return rc;
+        tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
+        bool vec = TQ >= 4 && (tp.in_stride % 4) == 0 && ((uintptr_t)in % 16) == 0 &&
+                   (!above || ((uintptr_t)above % 16) == 0) &&
+                   (!below || ((uintptr_t)below % 16) == 0);
+        return vec ? launch_tile<kPackedVec>(tp, rows, st)
+                   : launch_tile<kPackedScalar>(tp, rows, st);
+    }
+    if (in_stride < w) return fail(BE_EINVAL, "input row stride %lld bytes < width %lld",
+                                   (long long)in_stride, (long long)w);
+    tp.in_stride = in_stride;
+    bool vec = (in_stride % 16) == 0 && ((uintptr_t)in % 16) == 0 &&
+               (!above || ((uintptr_t)above % 16) == 0) && (!below || ((uintptr_t)below % 16) == 0);
+    return vec ? launch_tile<kU8Vec>(tp, rows, st) : launch_tile<kU8Byte>(tp, rows, st);
+}
+
+// ---------------------------------------------------------------- small kernels
+
+struct WordGeom {
+    int64_t nrows, stride;  // uint32 units
+    int wp, pl, swap;
+    uint32_t lastbit, padmask, fillword;
+    int64_t h;
+};
+
+WordGeom word_geom(const Geometry &G, int64_t stride_words) {
+    WordGeom g;
+    g.nrows = G.n * G.h;
+    g.stride = G.word_bits == 64 ? 2 * stride_words : stride_words;
+    g.wp = G.wp; g.pl = G.pl; g.swap = G.swap;
+    g.lastbit = G.lastbit; g.padmask = G.padmask; g.fillword = G.fillword;
+    g.h = G.h;
+    return g;
+}
+
+__device__ __forceinline__ uint32_t force_pad(const WordGeom &g, int pw, uint32_t v) {
+    if (pw == g.pl) return v | g.padmask;
+    if (pw > g.pl) return 0xFFFFFFFFu;
+    return v;
+}
+
+// invert / AND / OR (bitimage.py:181-205), padding re-forced to 1.
+__global__ void bitop_kernel(int op, const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                             uint32_t *__restrict__ out, WordGeom g) {
+    const int64_t total = g.nrows * g.wp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / g.wp;
+        const int m = (int)(t - row * g.wp);
+        const int64_t o = row * g.stride + m;
+        uint32_t v = a[o];
+        if (op == BE_OP_NOT) v = ~v;
+        else if (op == BE_OP_AND) v &= b[o];
+        else v |= b[o];
+        out[o] = force_pad(g, m ^ g.swap, v);
+    }
+}
+
+// Word of the shifted raster (bitimage.py:207-240); pw = pixel word, row = global row.
+__device__ __forceinline__ uint32_t shifted_word(const uint32_t *__restrict__ in, const WordGeom &g,
+                                                 int64_t row, int pw, int dir) {
+    const uint32_t *r = in + row * g.stride;
+    const int64_t y = row % g.h;
+    switch (dir) {
+        case BE_DOWN:   // out(y) = in(y-1): row 0 <- fill
+            return y == 0 ? g.fillword : r[-g.stride + (pw ^ g.swap)];
+        case BE_UP:     // out(y) = in(y+1): last row <- fill
+            return y == g.h - 1 ? g.fillword : r[g.stride + (pw ^ g.swap)];
+        case BE_RIGHT: {  // out(x) = in(x-1): pixel 0 <- fill
+            const uint32_t c = r[pw ^ g.swap];
+            const uint32_t l = pw == 0 ? g.fillword : r[(pw - 1) ^ g.swap];
+            return __funnelshift_r(c, l, 1);
+        }
+        default: {      // BE_LEFT, out(x) = in(x+1): pixel w-1 <- fill
+            if (pw > g.pl) return 0xFFFFFFFFu;
+            const uint32_t c = r[pw ^ g.swap];
+            const uint32_t rr = pw + 1 < g.wp ? r[(pw + 1) ^ g.swap] : 0u;
+            uint32_t v = __funnelshift_l(rr, c, 1);
+            if (pw == g.pl) v = (v & ~g.lastbit) | (g.fillword & g.lastbit);
+            return v;
+        }
+    }
+}
+
+__global__ void shift_kernel(const uint32_t *__restrict__ in, const uint32_t *__restrict__ mask,
+                             uint32_t *__restrict__ out, WordGeom g, int dir) {
+    const int64_t total = g.nrows * g.wp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / g.wp;
+        const int pw = (int)(t - row * g.wp);
+        uint32_t v = shifted_word(in, g, row, pw, dir);
+        const int64_t o = row * g.stride + (pw ^ g.swap);
+        if (mask) v &= mask[o];
+        out[o] = force_pad(g, pw, v);
+    }
+}
+
+__global__ void count_black_kernel(const uint32_t *__restrict__ in, unsigned long long *counts,
+                                   WordGeom g) {
+    const int64_t total = g.nrows * g.wp;
+    unsigned long long acc = 0;
+    int64_t cur_img = -1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / g.wp;
+        const int pw = (int)(t - row * g.wp);
+        if (pw > g.pl) continue;
+        uint32_t black = ~in[row * g.stride + (pw ^ g.swap)];
+        if (pw == g.pl) black &= ~g.padmask;
+        const int64_t img = row / g.h;
+        if (img != cur_img) {
+            if (cur_img >= 0 && acc) atomicAdd(counts + cur_img, acc);
+            cur_img = img;
+            acc = 0;
+        }
+        acc += __popc(black);
+    }
+    if (cur_img >= 0 && acc) atomicAdd(counts + cur_img, acc);
+}
+
+// to_array (bitimage.py:149-153): one thread per pixel word -> 32 bytes.
+__global__ void unpack_kernel(const uint32_t *__restrict__ in, uint8_t *__restrict__ out,
+                              WordGeom g, int64_t w, int64_t out_stride) {
+    const int64_t total = g.nrows * (int64_t)(g.pl + 1);
+    const int wpix = g.pl + 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / wpix;
+        const int pw = (int)(t - row * wpix);
+        const uint32_t v = in[row * g.stride + (pw ^ g.swap)];
+        uint8_t *o = out + row * out_stride + (int64_t)pw * 32;
+        const int64_t x0 = (int64_t)pw * 32;
+        if (x0 + 32 <= w && ((uintptr_t)o % 16) == 0) {
+            uint32_t q[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t nib = (v >> (28 - 4 * k)) & 0xFu;   // pixels 4k..4k+3
+                q[k] = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) |
+                       ((nib & 1u) << 24);
+            }
+            reinterpret_cast<uint4 *>(o)[0] = make_uint4(q[0], q[1], q[2], q[3]);
+            reinterpret_cast<uint4 *>(o)[1] = make_uint4(q[4], q[5], q[6], q[7]);
+        } else {
+            for (int b = 0; b < 32 && x0 + b < w; ++b) o[b] = (v >> (31 - b)) & 1u;
+        }
+    }
+}
+
+// detect_edges_scan: per-pixel Edge(p), one bit at a time.
+__device__ __forceinline__ uint32_t pixel_at(const uint32_t *__restrict__ in, const WordGeom &g,
+                                             int64_t img_row0, int64_t x, int64_t y, int64_t w) {
+    if (x < 0 || y < 0 || x >= w || y >= g.h) return g.fillword & 1u;
+    const int64_t row = img_row0 + y;
+    const int pw = (int)(x >> 5);
+    return (in[row * g.stride + (pw ^ g.swap)] >> (31 - (x & 31))) & 1u;
+}
+
+__global__ void scan_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, WordGeom g,
+                            int64_t w) {
+    const int64_t total = g.nrows * g.wp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / g.wp;
+        const int pw = (int)(t - row * g.wp);
+        const int64_t y = row % g.h, r0 = row - y;
+        uint32_t word = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int64_t x = (int64_t)pw * 32 + b;
+            uint32_t bit = 1u;
+            if (x < w) {
+                const uint32_t p = pixel_at(in, g, r0, x, y, w);
+                const uint32_t nb = pixel_at(in, g, r0, x, y - 1, w) |      // Fig. 1 n2
+                                    pixel_at(in, g, r0, x - 1, y, w) |      // n4
+                                    pixel_at(in, g, r0, x, y + 1, w) |      // n6
+                                    pixel_at(in, g, r0, x + 1, y, w);       // n8
+                bit = !(!p && nb);
+            }
+            word = (word << 1) | bit;
+        }
+        out[row * g.stride + (pw ^ g.swap)] = word;
+    }
+}
+
+unsigned grid_for(int64_t total) {
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = 148 * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (unsigned)blocks;
+}
+
+int prep_words(Geometry &G, int word_bits, int64_t n, int64_t h, int64_t w, int64_t stride,
+               int fill_bit, const void *a, const char *aname, const void *out) {
+    int rc = make_geometry(G, word_bits, n, h, w, fill_bit);
+    if (rc) return rc;
+    if ((rc = check_stride(G, stride, "row"))) return rc;
+    if (n == 0) return BE_OK;
+    if ((rc = check_ptr(a, word_bits, aname))) return rc;
+    if ((rc = check_ptr(out, word_bits, "output"))) return rc;
+    return BE_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+
+extern "C" {
+
+const char *be_last_error(void) { return g_err; }
+int be_abi_version(void) { return BE_ABI_VERSION; }
+int64_t be_launch_count(void) { return g_launches; }
+
+int be_edges_general(const void *in, int input_kind, int64_t in_row_stride,
+                     const void *above_or_null, const void *below_or_null, const be_outputs *outs,
+                     int word_bits, int64_t out_row_stride_words, int64_t n, int64_t h, int64_t w,
+                     int fill_bit, int64_t row_lo, int64_t row_hi, void *stream) {
+    if (outs == nullptr) return fail(BE_EINVAL, "outputs is NULL");
+    uint32_t *side[4] = {(uint32_t *)outs->side[0], (uint32_t *)outs->side[1],
+                         (uint32_t *)outs->side[2], (uint32_t *)outs->side[3]};
+    return edges_impl(in, input_kind, in_row_stride, above_or_null, below_or_null,
+                      (uint32_t *)outs->edges, (uint32_t *)outs->edgeset, side,
+                      (uint32_t *)outs->packed, word_bits, out_row_stride_words, n, h, w, fill_bit,
+                      row_lo, row_hi, stream);
+}
+
+static int edge_packed(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                       int64_t stride, int fill_bit, int emit_edgeset, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t *o = (uint32_t *)out;
+    return edges_impl(in, 0, stride, nullptr, nullptr, emit_edgeset ? nullptr : o,
+                      emit_edgeset ? o : nullptr, side, nullptr, word_bits, stride, n, h, w,
+                      fill_bit, 0, n * h, stream);
+}
+
+int be_edge_packed_u32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream) {
+    return edge_packed(in, out, 32, n, h, w, row_stride_words, fill_bit, emit_edgeset, stream);
+}
+
+int be_edge_packed_u64(const uint64_t *in, uint64_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream) {
+    return edge_packed(in, out, 64, n, h, w, row_stride_words, fill_bit, emit_edgeset, stream);
+}
+
+int be_pack_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int fill_bit,
+                    uint32_t *packed_in_or_null, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, packed_in_or_null,
+                      32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream);
+}
+
+int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
+                            const uint32_t *below_or_null, uint32_t *out, int64_t rows, int64_t w,
+                            int64_t row_stride_words, int fill_bit, int64_t row_lo, int64_t row_hi,
+                            void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(slab, 0, row_stride_words, above_or_null, below_or_null, out, nullptr, side,
+                      nullptr, 32, row_stride_words, 1, rows, w, fill_bit, row_lo, row_hi, stream);
+}
+
+int be_pack_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+               int64_t in_row_stride, int64_t out_row_stride_words, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
+                      (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
+                      stream);
+}
+
+int be_unpack_u8(const void *in, uint8_t *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                 int64_t in_row_stride_words, int64_t out_row_stride, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, 1);
+    if (rc) return rc;
+    if ((rc = check_stride(G, in_row_stride_words, "input"))) return rc;
+    if (out_row_stride < w) return fail(BE_EINVAL, "output row stride < width");
+    if (n == 0) return BE_OK;
+    if ((rc = check_ptr(in, word_bits, "input"))) return rc;
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    WordGeom g = word_geom(G, in_row_stride_words);
+    unpack_kernel<<<grid_for(g.nrows * (g.pl + 1)), 256, 0, S(stream)>>>(
+        (const uint32_t *)in, out, g, w, out_row_stride);
+    return cuda_check("unpack_kernel");
+}
+
+int be_bitop(int op, const void *a, const void *b, void *out, int word_bits, int64_t n, int64_t h,
+             int64_t w, int64_t row_stride_words, void *stream) {
+    Geometry G;
+    if (op != BE_OP_NOT && op != BE_OP_AND && op != BE_OP_OR)
+        return fail(BE_EINVAL, "unknown op %d", op);
+    int rc = prep_words(G, word_bits, n, h, w, row_stride_words, 1, a, "operand a", out);
+    if (rc || n == 0) return rc;
+    if (op != BE_OP_NOT && (rc = check_ptr(b, word_bits, "operand b"))) return rc;
+    WordGeom g = word_geom(G, row_stride_words);
+    bitop_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
+        op, (const uint32_t *)a, (const uint32_t *)b, (uint32_t *)out, g);
+    return cuda_check("bitop_kernel");
+}
+
+int be_shift(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+             int64_t row_stride_words, int direction, int fill_bit, void *stream) {
+    Geometry G;
+    if (direction < BE_LEFT || direction > BE_DOWN)
+        return fail(BE_EINVAL, "unknown direction %d", direction);
+    int rc = prep_words(G, word_bits, n, h, w, row_stride_words, fill_bit, in, "input", out);
+    if (rc || n == 0) return rc;
+    if (in == out) return fail(BE_EINVAL, "output aliases the input");
+    WordGeom g = word_geom(G, row_stride_words);
+    shift_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
+        (const uint32_t *)in, nullptr, (uint32_t *)out, g, direction);
+    return cuda_check("shift_kernel");
+}
+
+int be_shift_and(const void *img, const void *mask, void *out, int word_bits, int64_t n,
+                 int64_t h, int64_t w, int64_t row_stride_words, int side, int fill_bit,
+                 void *stream) {
+    Geometry G;
+    if (side < BE_LEFT || side > BE_DOWN) return fail(BE_EINVAL, "unknown side %d", side);
+    int rc = prep_words(G, word_bits, n, h, w, row_stride_words, fill_bit, img, "image", out);
+    if (rc || n == 0) return rc;
+    if ((rc = check_ptr(mask, word_bits, "mask"))) return rc;
+    if (img == out) return fail(BE_EINVAL, "output aliases the input");
+    static const int opposite[4] = {BE_RIGHT, BE_LEFT, BE_DOWN, BE_UP};
+    WordGeom g = word_geom(G, row_stride_words);
+    shift_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
+        (const uint32_t *)img, (const uint32_t *)mask, (uint32_t *)out, g, opposite[side]);
+    return cuda_check("shift_kernel");
+}
+
+int be_count_black(const void *in, int64_t *counts, int word_bits, int64_t n, int64_t h,
+                   int64_t w, int64_t row_stride_words, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, 1);
+    if (rc) return rc;
+    if ((rc = check_stride(G, row_stride_words, "row"))) return rc;
+    if (n == 0) return BE_OK;
+    if ((rc = check_ptr(in, word_bits, "input"))) return rc;
+    if (counts == nullptr || ((uintptr_t)counts % 8)) return fail(BE_EINVAL, "bad counts pointer");
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * n, S(stream));
+    if (e != cudaSuccess) return fail((int)e, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+    WordGeom g = word_geom(G, row_stride_words);
+    count_black_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
+        (const uint32_t *)in, (unsigned long long *)counts, g);
+    return cuda_check("count_black_kernel");
+}
+
+int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                  int64_t row_stride_words, int fill_bit, void *stream) {
+    Geometry G;
+    int rc = prep_words(G, word_bits, n, h, w, row_stride_words, fill_bit, in, "input", out);
+    if (rc || n == 0) return rc;
+    if (in == out) return fail(BE_EINVAL, "output aliases the input");
+    WordGeom g = word_geom(G, row_stride_words);
+    scan_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
+        (const uint32_t *)in, (uint32_t *)out, g, w);
+    return cuda_check("scan_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,353 @@
+"""Tensor API over device-resident batches (`bitedge.cuda`).
+
+The reference has no batch type (`from_array` is 2-d only, bitimage.py:126-127);
+this is the surface the benchmarks and the multi-GPU layer call.  Every
+function launches hand-written sm_100a kernels through the C ABI
+(include/bitedge.h) on the current torch stream; there is no CPU path.
+
+Packed rasters are integer tensors of shape [N, H, S] or [H, S]:
+  int32 / uint32  -> 32-bit MSB-first row words (BASELINE configs 3 and 4);
+  int64 / uint64  -> the reference's native uint64 words (BitImage.words).
+S is the row length in words (>= ceil(W / word_bits)); the last dimension
+must be contiguous and images contiguous.  Pixel inputs are uint8 / int8 /
+bool [N, H, W] (any nonzero byte is white, bitimage.py:124, 133).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _capi
+
+WHITE_OUTSIDE = 1
+BLACK_OUTSIDE = 0
+
+_WORD_DTYPES = {torch.int32: 32, torch.int64: 64}
+for _name, _bits in (("uint32", 32), ("uint64", 64)):
+    if hasattr(torch, _name):
+        _WORD_DTYPES[getattr(torch, _name)] = _bits
+_PIXEL_DTYPES = (torch.uint8, torch.int8, torch.bool)
+
+
+def fill_bit(border) -> int:
+    """BorderPolicy (bitimage.py:56-64) or 0/1 -> fill bit."""
+    v = getattr(border, "value", border)
+    if v not in (0, 1) or isinstance(v, float):
+        raise ValueError(f"border must be a BorderPolicy or 0/1, got {border!r}")
+    return int(v)
+
+
+def _require_cuda(t: torch.Tensor, what: str) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (there is no CPU path)")
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _as3d(t: torch.Tensor, what: str) -> torch.Tensor:
+    if t.dim() == 2:
+        return t.unsqueeze(0)
+    if t.dim() == 3:
+        return t
+    raise ValueError(f"{what} must be [H, S] or [N, H, S], got shape {tuple(t.shape)}")
+
+
+def _row_stride(t3: torch.Tensor, what: str) -> int:
+    n, h, s = t3.shape
+    if s and t3.stride(2) != 1:
+        raise ValueError(f"{what}: rows must be contiguous")
+    rs = t3.stride(1) if h > 1 else max(s, t3.stride(1))
+    if n > 1 and t3.stride(0) != h * rs:
+        raise ValueError(f"{what}: images of a batch must be contiguous")
+    return rs
+
+
+def word_bits_of(t: torch.Tensor) -> int:
+    try:
+        return _WORD_DTYPES[t.dtype]
+    except KeyError:
+        raise ValueError(f"packed words must be int32/uint32/int64/uint64, got {t.dtype}") from None
+
+
+def words_per_row(width: int, word_bits: int = 32) -> int:
+    return -(-int(width) // word_bits)
+
+
+def _packed(words: torch.Tensor, width: int, what: str = "words"):
+    _require_cuda(words, what)
+    wb = word_bits_of(words)
+    w3 = _as3d(words, what)
+    rs = _row_stride(w3, what)
+    if w3.shape[2] < words_per_row(width, wb):
+        raise ValueError(f"{what}: width {width} needs {words_per_row(width, wb)} words per row, "
+                         f"got {w3.shape[2]}")
+    return w3, wb, rs
+
+
+def _new_like(w3: torch.Tensor, squeeze: bool) -> torch.Tensor:
+    out = torch.empty(w3.shape, dtype=w3.dtype, device=w3.device)
+    return out[0] if squeeze else out
+
+
+def _check_out(out: torch.Tensor, ref3: torch.Tensor, squeeze: bool, what="out"):
+    _require_cuda(out, what)
+    o3 = _as3d(out, what)
+    if o3.shape != ref3.shape or o3.dtype != ref3.dtype:
+        raise ValueError(f"{what} must have shape {tuple(ref3.shape)} and dtype {ref3.dtype}")
+    return o3
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+# ------------------------------------------------------------------ hot path
+
+def edges_packed(words: torch.Tensor, width: int, border=WHITE_OUTSIDE, *, out=None,
+                 edgeset: bool = False) -> torch.Tensor:
+    """detect_edges_mask -- or the EdgeSet
+    when `edgeset` -- of packed rasters, in one fused pass (kernel K1)."""
+    squeeze = words.dim() == 2
+    w3, wb, rs = _packed(words, width)
+    o = _new_like(w3, squeeze) if out is None else out
+    o3 = _check_out(o, w3, squeeze)
+    if _row_stride(o3, "out") != rs:
+        raise ValueError("out must have the input's row stride")
+    n, h, _ = w3.shape
+    name = "be_edge_packed_u64" if wb == 64 else "be_edge_packed_u32"
+    _capi.call(name, _ptr(w3), _ptr(o3), n, h, int(width), rs, fill_bit(border), int(edgeset),
+               ctypes.c_void_p(_stream(w3)))
+    return o
+
+
+def _pixels(pixels: torch.Tensor, what="pixels"):
+    _require_cuda(pixels, what)
+    if pixels.dtype not in _PIXEL_DTYPES:
+        raise ValueError(f"{what} must be uint8/int8/bool (nonzero = white), got {pixels.dtype}")
+    p3 = _as3d(pixels, what)
+    if p3.shape[2] < 1 or p3.shape[1] < 1:
+        raise ValueError(f"image dimensions must be at least 1x1, got {p3.shape[2]}x{p3.shape[1]}")
+    return p3, _row_stride(p3, what)
+
+
+def pack_edges_u8(pixels: torch.Tensor, border=WHITE_OUTSIDE, *, out=None,
+                  packed_out: torch.Tensor | None = None) -> torch.Tensor:
+    """from_array + detect_edges_mask fused (kernel K2): uint8 [N,H,W] ->
+    int32 [N,H,ceil(W/32)] MSB-first edge words.  `packed_out` (same shape)
+    additionally receives the packed input."""
+    squeeze = pixels.dim() == 2
+    p3, prs = _pixels(pixels)
+    n, h, w = p3.shape
+    shape = (n, h, words_per_row(w, 32))
+    o = out if out is not None else torch.empty(shape, dtype=torch.int32, device=p3.device)
+    o3 = _as3d(o, "out")
+    _require_cuda(o3, "out")
+    if tuple(o3.shape) != shape or word_bits_of(o3) != 32:
+        raise ValueError(f"out must be 32-bit words of shape {shape}")
+    ors = _row_stride(o3, "out")
+    pk = None
+    if packed_out is not None:
+        pk = _as3d(packed_out, "packed_out")
+        if tuple(pk.shape) != shape or word_bits_of(pk) != 32 or _row_stride(pk, "packed_out") != ors:
+            raise ValueError("packed_out must match out")
+    _capi.call("be_pack_edge_u8", _ptr(p3), _ptr(o3), n, h, w, prs, ors, fill_bit(border), _ptr(pk),
+               ctypes.c_void_p(_stream(p3)))
+    return o[0] if (squeeze and out is None) else o
+
+
+def edges_general(inp: torch.Tensor, width: int | None = None, border=WHITE_OUTSIDE, *,
+                  word_bits: int = 32, edges=True, edgeset=False, sides=False, packed=False,
+                  above=None, below=None, row_lo: int = 0, row_hi: int | None = None,
+                  outs: dict | None = None) -> dict:
+    """Every output of the fused kernel from one read of the input (F3):
+    'edges', 'edgeset', 'left'/'right'/'up'/'down' fundamental edges
+     and 'packed'.  `inp` is packed words or uint8 pixels."""
+    _require_cuda(inp, "input")
+    if inp.dtype in _PIXEL_DTYPES:
+        p3, irs = _pixels(inp, "input")
+        kind = 1
+        n, h, width = p3.shape
+        wb = word_bits
+        src = p3
+    else:
+        if width is None:
+            raise ValueError("width is required for packed input")
+        src, wb, irs = _packed(inp, width, "input")
+        kind = 0
+        n, h, _ = src.shape
+    shape = (n, h, words_per_row(width, wb))
+    dt = torch.int64 if wb == 64 else torch.int32
+    names = []
+    if edges:
+        names.append("edges")
+    if edgeset:
+        names.append("edgeset")
+    if sides:
+        names += ["left", "right", "up", "down"]
+    if packed:
+        names.append("packed")
+    res = dict(outs or {})
+    for k in names:
+        if k not in res:
+            res[k] = torch.empty(shape, dtype=dt, device=src.device)
+    ors = None
+    for k, v in res.items():
+        v3 = _as3d(v, k)
+        if tuple(v3.shape) != shape or word_bits_of(v3) != wb:
+            raise ValueError(f"output {k} must be {wb}-bit words of shape {shape}")
+        r = _row_stride(v3, k)
+        if ors is None:
+            ors = r
+        elif r != ors:
+            raise ValueError("all outputs must share one row stride")
+    o = _capi.be_outputs()
+    o.edges = res["edges"].data_ptr() if "edges" in res else None
+    o.edgeset = res["edgeset"].data_ptr() if "edgeset" in res else None
+    for i, k in enumerate(("left", "right", "up", "down")):
+        o.side[i] = res[k].data_ptr() if k in res else None
+    o.packed = res["packed"].data_ptr() if "packed" in res else None
+    if row_hi is None:
+        row_hi = n * h
+    _capi.call("be_edges_general", _ptr(src), kind, irs, _ptr(above), _ptr(below),
+               ctypes.byref(o), wb, ors, n, h, int(width), fill_bit(border), int(row_lo),
+               int(row_hi), ctypes.c_void_p(_stream(src)))
+    return res
+
+
+def edges_halo(slab: torch.Tensor, above, below, width: int, border=WHITE_OUTSIDE, *, out=None,
+               row_lo: int = 0, row_hi: int | None = None) -> torch.Tensor:
+    """Kernel K3: edges of a row slab [rows, S] (int32 words) whose row -1 /
+    row `rows` are the neighbour slabs' boundary rows (`above` / `below`,
+    [S] tensors with the slab's stride, or None at the image border)."""
+    _require_cuda(slab, "slab")
+    if slab.dim() != 2 or word_bits_of(slab) != 32:
+        raise ValueError("slab must be a 2-d 32-bit word tensor")
+    w3, wb, rs = _packed(slab, width, "slab")
+    rows = slab.shape[0]
+    for t, nm in ((above, "above"), (below, "below")):
+        if t is not None:
+            _require_cuda(t, nm)
+            if t.dtype != slab.dtype or t.numel() < slab.shape[1] or t.stride(-1) != 1:
+                raise ValueError(f"{nm} must be one contiguous row of the slab's dtype")
+    o = torch.empty_like(slab) if out is None else out
+    if o.shape != slab.shape or o.dtype != slab.dtype or o.stride() != slab.stride():
+        raise ValueError("out must match the slab")
+    if row_hi is None:
+        row_hi = rows
+    _capi.call("be_edge_packed_halo_u32", _ptr(slab), _ptr(above), _ptr(below), _ptr(o), rows,
+               int(width), rs, fill_bit(border), int(row_lo), int(row_hi),
+               ctypes.c_void_p(_stream(slab)))
+    return o
+
+
+# ------------------------------------------------------------------ primitives
+
+def pack_u8(pixels: torch.Tensor, word_bits: int = 32, out=None) -> torch.Tensor:
+    """BitImage.from_array (bitimage.py:122-136) on the device."""
+    squeeze = pixels.dim() == 2
+    p3, prs = _pixels(pixels)
+    n, h, w = p3.shape
+    shape = (n, h, words_per_row(w, word_bits))
+    dt = torch.int64 if word_bits == 64 else torch.int32
+    o = out if out is not None else torch.empty(shape, dtype=dt, device=p3.device)
+    o3 = _as3d(o, "out")
+    if tuple(o3.shape) != shape or word_bits_of(o3) != word_bits:
+        raise ValueError(f"out must be {word_bits}-bit words of shape {shape}")
+    _capi.call("be_pack_u8", _ptr(p3), _ptr(o3), word_bits, n, h, w, prs, _row_stride(o3, "out"),
+               ctypes.c_void_p(_stream(p3)))
+    return o[0] if (squeeze and out is None) else o
+
+
+def unpack_u8(words: torch.Tensor, width: int, out=None) -> torch.Tensor:
+    """BitImage.to_array (bitimage.py:149-153) on the device: uint8 {0,1}."""
+    squeeze = words.dim() == 2
+    w3, wb, rs = _packed(words, width)
+    n, h, _ = w3.shape
+    o = out if out is not None else torch.empty((n, h, int(width)), dtype=torch.uint8,
+                                                device=w3.device)
+    o3 = _as3d(o, "out")
+    if tuple(o3.shape) != (n, h, int(width)) or o3.dtype != torch.uint8:
+        raise ValueError("out must be uint8 [N, H, W]")
+    _capi.call("be_unpack_u8", _ptr(w3), _ptr(o3), wb, n, h, int(width), rs,
+               _row_stride(o3, "out"), ctypes.c_void_p(_stream(w3)))
+    return o[0] if (squeeze and out is None) else o
+
+
+def _binary(name, op, a, b, width):
+    squeeze = a.dim() == 2
+    a3, wb, rs = _packed(a, width, "a")
+    b3 = None
+    if b is not None:
+        b3, wb2, rs2 = _packed(b, width, "b")
+        if b3.shape != a3.shape or wb2 != wb or rs2 != rs:
+            raise ValueError("operands must have identical shape, dtype and stride")
+    o = _new_like(a3, squeeze)
+    o3 = _as3d(o, "out")
+    n, h, _ = a3.shape
+    _capi.call("be_bitop", op, _ptr(a3), _ptr(b3), _ptr(o3), wb, n, h,
+               int(width), rs, ctypes.c_void_p(_stream(a3)))
+    return o
+
+
+def invert(words, width):
+    return _binary("invert", _capi.BE_OP_NOT, words, None, width)
+
+
+def and_(a, b, width):
+    return _binary("and", _capi.BE_OP_AND, a, b, width)
+
+
+def or_(a, b, width):
+    return _binary("or", _capi.BE_OP_OR, a, b, width)
+
+
+def shift(words, width, direction: int, border=WHITE_OUTSIDE):
+    """BitImage.shift (bitimage.py:207-240); direction BE_LEFT..BE_DOWN."""
+    squeeze = words.dim() == 2
+    w3, wb, rs = _packed(words, width)
+    o = _new_like(w3, squeeze)
+    n, h, _ = w3.shape
+    _capi.call("be_shift", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs, int(direction),
+               fill_bit(border), ctypes.c_void_p(_stream(w3)))
+    return o
+
+
+def shift_and(img, mask, width, side: int, border=WHITE_OUTSIDE):
+    """fundamental_edge(img, mask, side) = shift(img, opposite(side)) & mask, fused."""
+    squeeze = img.dim() == 2
+    i3, wb, rs = _packed(img, width, "img")
+    m3, wb2, rs2 = _packed(mask, width, "mask")
+    if m3.shape != i3.shape or wb2 != wb or rs2 != rs:
+        raise ValueError("img and mask must have identical shape, dtype and stride")
+    o = _new_like(i3, squeeze)
+    n, h, _ = i3.shape
+    _capi.call("be_shift_and", _ptr(i3), _ptr(m3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
+               int(side), fill_bit(border), ctypes.c_void_p(_stream(i3)))
+    return o
+
+
+def count_black(words, width) -> torch.Tensor:
+    """BitImage.count_black (bitimage.py:244-249) per image: int64 [N]."""
+    w3, wb, rs = _packed(words, width)
+    n, h, _ = w3.shape
+    counts = torch.empty(n, dtype=torch.int64, device=w3.device)
+    _capi.call("be_count_black", _ptr(w3), _ptr(counts), wb, n, h, int(width), rs,
+               ctypes.c_void_p(_stream(w3)))
+    return counts
+
+
+def scan_edges(words, width, border=WHITE_OUTSIDE):
+    """detect_edges_scan: per-pixel Edge(p) on the device."""
+    squeeze = words.dim() == 2
+    w3, wb, rs = _packed(words, width)
+    o = _new_like(w3, squeeze)
+    n, h, _ = w3.shape
+    _capi.call("be_scan_edges", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
+               fill_bit(border), ctypes.c_void_p(_stream(w3)))
+    return o

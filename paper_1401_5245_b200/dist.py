@@ -1,0 +1,116 @@
+"""Multi-GPU layer: one process per GPU over torch.distributed (NCCL on the
+B200 box, gloo in the CPU tests).  The reference is single-threaded numpy
+with no distributed code; this layer is new.
+
+* Batch sharding (configs C2, C5): rank r owns images [lo, hi) of the batch
+  (`shard_range`); the images are independent, so there is no collective on
+  the data path.
+* Row sharding (config C4): rank r owns rows [lo, hi) of one giant raster.
+  The only exchange is one packed row to each row neighbour (`exchange_halos`,
+  grouped NCCL send/recv over NVLink, 8 KiB per message at 65536 px).  The
+  interior rows, which need no halo, are computed while the exchange is in
+  flight; the two boundary rows follow with the received halos (kernel K3).
+  Ranks 0 and G-1 use the border fill on their outer side (bitimage.py:216-223).
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [lo, hi) of `total` units for `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def env_rank_world() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: str | None = None) -> tuple[int, int]:
+    """Initialise the default process group from torchrun's env (no-op at world 1)."""
+    rank, world, local = env_rank_world()
+    if world > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world
+
+
+def exchange_halos(first_row: torch.Tensor, last_row: torch.Tensor, above: torch.Tensor,
+                   below: torch.Tensor, rank: int, world: int, group=None):
+    """Post the halo exchange of one row slab and return the pending works.
+
+    Sends `first_row` to rank-1 and `last_row` to rank+1; receives rank-1's
+    last row into `above` and rank+1's first row into `below`.  At the image
+    border (rank 0 above, rank world-1 below) nothing is exchanged and the
+    caller passes a NULL halo so the kernel applies the border fill."""
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.irecv, above, rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, first_row, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.irecv, below, rank + 1, group))
+        ops.append(dist.P2POp(dist.isend, last_row, rank + 1, group))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+class RowShardedEdges:
+    """Edges of this rank's row slab of one raster (config C4), with the halo
+    exchange overlapped with the interior rows.
+
+    `slab` is an int32 CUDA tensor [rows, S] of MSB-first row words; the
+    result lands in `self.out` (same shape)."""
+
+    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None):
+        from . import cuda as _cuda
+
+        self._cuda = _cuda
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.group = group
+        self.slab = slab
+        self.width = int(width)
+        self.border = border
+        self.rows = slab.shape[0]
+        s = slab.shape[1]
+        # halo buffers padded to a 16-byte multiple so the kernel's 128-bit loads stay in bounds
+        pad = (s + 3) // 4 * 4
+        self.above = torch.empty(pad, dtype=slab.dtype, device=slab.device)
+        self.below = torch.empty(pad, dtype=slab.dtype, device=slab.device)
+        self.out = torch.empty_like(slab)
+
+    def step(self) -> torch.Tensor:
+        cu, rows = self._cuda, self.rows
+        works = exchange_halos(self.slab[0], self.slab[rows - 1], self.above[: self.slab.shape[1]],
+                               self.below[: self.slab.shape[1]], self.rank, self.world, self.group)
+        above = self.above if self.rank > 0 else None
+        below = self.below if self.rank < self.world - 1 else None
+        if not works:
+            cu.edges_halo(self.slab, None, None, self.width, self.border, out=self.out)
+            return self.out
+        if rows > 2:  # interior rows need no halo: overlap them with the exchange
+            cu.edges_halo(self.slab, None, None, self.width, self.border, out=self.out,
+                          row_lo=1, row_hi=rows - 1)
+        for w in works:
+            w.wait()
+        cu.edges_halo(self.slab, above, below, self.width, self.border, out=self.out,
+                      row_lo=0, row_hi=1)
+        if rows > 1:
+            cu.edges_halo(self.slab, above, below, self.width, self.border, out=self.out,
+                          row_lo=rows - 1, row_hi=rows)
+        return self.out

@@ -1,0 +1,371 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the golden vectors the real reference produced.  Bit-exact on every word,
+padding included.  Run with `pytest -m gpu` on a B200."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import encode_bits, exhaustive_images, golden, split_corpus
+from oracle import cscan
+from oracle import port as P
+
+pytestmark = pytest.mark.gpu
+
+POL = {"WHITE_OUTSIDE": 1, "BLACK_OUTSIDE": 0}
+
+
+def _t(a, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+# ---------------------------------------------------------------- exhaustive (SPEC acceptance 1)
+
+@pytest.mark.parametrize("n", [3, 4])
+@pytest.mark.parametrize("pol", list(POL))
+def test_exhaustive_batch_u8(cuda_dev, n, pol):
+    """All 2^(n*n) rasters as ONE batch through the fused pack+edge kernel."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    g = golden("exhaustive.npz")
+    imgs = exhaustive_images(n)
+    fill = POL[pol]
+    out = cu.pack_edges_u8(_t(imgs, cuda_dev), fill)
+    bits = P.unpack_u32(_u32(out), n)
+    assert (encode_bits(bits) == g[f"out{n}_{pol}"]).all()
+    # padding of every output word is 1
+    assert ((_u32(out) & np.uint32((1 << (32 - n)) - 1)) == (1 << (32 - n)) - 1).all()
+    # packed-input path (K1, u32 and u64 words) and the EdgeSet
+    packed32 = _t(P.pack_u32(imgs).view(np.int32), cuda_dev)
+    assert (_u32(cu.edges_packed(packed32, n, fill)) == _u32(out)).all()
+    es = cu.edges_packed(packed32, n, fill, edgeset=True)
+    assert (encode_bits(P.unpack_u32(_u32(es), n)) == g[f"eset{n}_{pol}"]).all()
+    packed64 = cu.pack_u8(_t(imgs, cuda_dev), word_bits=64)
+    o64 = cu.edges_packed(packed64, n, fill)
+    exp64 = np.stack([P.detect_edges_mask(P.from_array(imgs[i]), fill).words
+                      for i in range(0, len(imgs), 257)])
+    assert (_u64(o64)[::257] == exp64).all()
+
+
+# ---------------------------------------------------------------- random corpus (acceptance 1c)
+
+def _corpus():
+    g = golden("random.npz")
+    pix, packed = split_corpus(g["shapes"], g["pixels"], g["packed"])
+    return g, pix, packed
+
+
+def test_random_corpus_bitimage_api(cuda_dev):
+    """The drop-in API (BitImage + edge module) vs reference words, per image."""
+    from paper_1401_5245_b200 import edge as E
+    from paper_1401_5245_b200.bitimage import BitImage, BorderPolicy, Direction, first_difference
+
+    g, pix, packed = _corpus()
+    outs = {p: split_corpus(g["shapes"], g["pixels"], g[f"out_{p}"])[1] for p in POL}
+    esets = {p: split_corpus(g["shapes"], g["pixels"], g[f"eset_{p}"])[1] for p in POL}
+    funds = {(s, p): split_corpus(g["shapes"], g["pixels"], g[f"fund_{s}_{p}"])[1]
+             for s in ("LEFT", "RIGHT", "UP", "DOWN") for p in POL}
+    for i, a in enumerate(pix):
+        img = BitImage.from_array(a)
+        assert (img.words == packed[i]).all(), i
+        for pol in POL:
+            b = BorderPolicy[pol]
+            out = E.detect_edges_mask(img, b)
+            assert (out.words == outs[pol][i]).all(), (i, pol)
+            if i % 7 == 0:
+                assert (E.edge_set(img, b).words == esets[pol][i]).all()
+                assert (E.detect_edges_scan(img, b).words == outs[pol][i]).all()
+                m = E.build_mask(img)
+                for s in ("LEFT", "RIGHT", "UP", "DOWN"):
+                    fe = E.fundamental_edge(img, m, Direction[s], b)
+                    assert (fe.words == funds[(s, pol)][i]).all(), (i, s, pol)
+                fes = E.fundamental_edges(img, b)
+                for s in ("LEFT", "RIGHT", "UP", "DOWN"):
+                    assert (fes[Direction[s]].words == funds[(s, pol)][i]).all()
+                assert (fes["edges"].words == outs[pol][i]).all()
+                assert first_difference(out, E.detect_edges_scan(img, b)) is None
+        if i % 50 == 0:
+            assert (img.to_array() == (a != 0)).all()
+
+
+def test_random_corpus_batched_u32(cuda_dev):
+    """Same corpus through the tensor API: u8 -> fused pack+edge and packed u32."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    g, pix, _ = _corpus()
+    outs = {p: split_corpus(g["shapes"], g["pixels"], g[f"out_{p}"])[1] for p in POL}
+    for i, a in enumerate(pix):
+        w = a.shape[1]
+        for pol, fill in POL.items():
+            exp = P.u64_to_u32_rows(outs[pol][i])[:, : -(-w // 32)]
+            got = _u32(cu.pack_edges_u8(_t(a, cuda_dev), fill))
+            assert (got == exp).all(), (i, pol)
+            if i % 5 == 0:
+                pk = _t(P.pack_u32(a).view(np.int32), cuda_dev)
+                assert (_u32(cu.edges_packed(pk, w, fill)) == exp).all()
+
+
+def test_first_difference_and_queries(cuda_dev):
+    from paper_1401_5245_b200.bitimage import BitImage, PixelColor, first_difference
+
+    a = BitImage.from_array(np.ones((5, 70), np.uint8))
+    b = a.set(66, 3, PixelColor.BLACK)
+    assert first_difference(a, b) == (66, 3)
+    assert b.count_black() == 1 and a.count_black() == 0
+    assert repr(b) == "BitImage(70x5, black=1)"
+    assert a != b and a == BitImage.filled(70, 5, PixelColor.WHITE)
+    assert b.to_text().splitlines()[3][66] == "#"
+
+
+# ---------------------------------------------------------------- primitives (acceptance 3)
+
+def test_primitives_vs_reference(cuda_dev):
+    from paper_1401_5245_b200.bitimage import BitImage, BorderPolicy, Direction
+
+    g = golden("shift.npz")
+    pix, _ = split_corpus(g["shapes"], g["pixels"])
+    exp = {k: split_corpus(g["shapes"], g["pixels"], g[k])[1] for k in g.files
+           if k.startswith("shift_") or k in ("invert", "and_rot", "or_rot")}
+    W, B = BorderPolicy.WHITE_OUTSIDE, BorderPolicy.BLACK_OUTSIDE
+    for i, a in enumerate(pix):
+        img = BitImage.from_array(a)
+        for s in ("LEFT", "RIGHT", "UP", "DOWN"):
+            for pol in POL:
+                got = img.shift(Direction[s], BorderPolicy[pol]).words
+                assert (got == exp[f"shift_{s}_{pol}"][i]).all(), (i, s, pol)
+        assert ((~img).words == exp["invert"][i]).all()
+        assert ((img & img.shift(Direction.RIGHT, W)).words == exp["and_rot"][i]).all()
+        assert ((img | img.shift(Direction.DOWN, B)).words == exp["or_rot"][i]).all()
+        assert img.count_black() == g["count_black"][i]
+
+
+def test_pack_rule_nonzero_bytes(cuda_dev):
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200.bitimage import BitImage
+
+    a = np.array([[0, 1, 2, 255, 0, 17, 128, 0]] * 3, dtype=np.uint8)
+    img = BitImage.from_array(a)
+    assert img.to_array().tolist() == [[0, 1, 1, 1, 0, 1, 1, 0]] * 3
+    assert BitImage.from_array(a.astype(np.int8)) == img
+    assert BitImage.from_array(a.astype(np.float32) * 0.5) == img
+    assert BitImage.from_array(a.astype(bool)) == img
+    t = torch.from_numpy(a).cuda()
+    assert (_u32(cu.pack_u8(t)) == P.pack_u32(a)).all()
+    assert (cu.unpack_u8(cu.pack_u8(t), 8).cpu().numpy() == (a != 0)).all()
+
+
+# ---------------------------------------------------------------- layouts / strides / alignment
+
+def test_strided_and_unaligned_inputs(cuda_dev):
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(11)
+    for (n, h, w) in [(3, 17, 45), (2, 9, 200), (1, 40, 1000), (5, 1, 33), (4, 33, 1)]:
+        a = (rng.random((n, h, w)) < 0.55).astype(np.uint8) * rng.integers(1, 256, (n, h, w)).astype(np.uint8)
+        exp = cscan.scan_u8(a, 1)
+        # contiguous, unaligned row stride (byte path)
+        assert (_u32(cu.pack_edges_u8(_t(a, cuda_dev), 1)) == exp).all(), (n, h, w)
+        # padded row stride (vector path) via a view into a wider buffer
+        wide = torch.zeros((n, h, (w + 15) // 16 * 16 + 16), dtype=torch.uint8, device=cuda_dev)
+        wide[..., :w] = _t(a, cuda_dev)
+        assert (_u32(cu.pack_edges_u8(wide[..., :w], 1)) == exp).all()
+        # packed words with a padded stride (scalar + vector paths)
+        pk = P.pack_u32(a)
+        for extra in (0, 1, 3, 4):
+            buf = np.full((n, h, pk.shape[2] + extra), 0xA5A5A5A5, dtype=np.uint32)
+            buf[..., : pk.shape[2]] = pk
+            t = _t(buf.view(np.int32), cuda_dev)[..., : pk.shape[2]]
+            assert (_u32(cu.edges_packed(t, w, 1)) == exp).all(), (n, h, w, extra)
+
+
+def test_garbage_padding_bits_ignored(cuda_dev):
+    """Inputs with padding bits 0 (or random) give the same output as pad = 1."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(5)
+    for w in (1, 5, 31, 33, 63, 65, 100, 129):
+        a = (rng.random((2, 7, w)) < 0.5).astype(np.uint8)
+        pk = P.pack_u32(a)
+        exp = cscan.scan_u8(a, 1)
+        noisy = pk ^ (rng.integers(0, 2**32, pk.shape, dtype=np.uint32)
+                      & np.uint32(P.u32_pad_mask(w) or 0))
+        noisy[..., :-1] = pk[..., :-1]
+        assert (_u32(cu.edges_packed(_t(noisy.view(np.int32), cuda_dev), w, 1)) == exp).all()
+        cleared = pk & ~np.uint32(P.u32_pad_mask(w))
+        assert (_u32(cu.edges_packed(_t(cleared.view(np.int32), cuda_dev), w, 0)) ==
+                cscan.scan_u8(a, 0)).all()
+
+
+# ---------------------------------------------------------------- BASELINE configs
+
+def test_config_c1(cuda_dev):
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+    from paper_1401_5245_b200.bitimage import BitImage, BorderPolicy
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    g = golden("configs.npz")
+    c1 = synth.c1_image()
+    img = BitImage.from_array(c1)
+    assert (img.words == g["c1_input_packed"]).all()
+    for pol in POL:
+        assert (detect_edges_mask(img, BorderPolicy[pol]).words == g[f"c1_out_{pol}"]).all()
+    got = _u32(cu.pack_edges_u8(_t(c1, cuda_dev), 1))
+    assert (got == P.u64_to_u32_rows(g["c1_out_WHITE_OUTSIDE"])).all()
+
+
+def test_config_c2_full(cuda_dev):
+    """4096 glyphs generated on the device; output digest == the reference's."""
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+
+    g = golden("configs.npz")
+    imgs = synth.c2_images(4096, device=cuda_dev)
+    assert hashlib.sha256(imgs.cpu().numpy().tobytes()).digest() == g["c2_in_sha256"].tobytes()
+    packed = torch_empty_like_words(imgs)
+    out = cu.pack_edges_u8(imgs, 1, packed_out=packed)
+    o = _u32(out)
+    assert hashlib.sha256(o.tobytes()).digest() == g["c2_out_sha256"].tobytes()
+    assert (o[:8] == P.u64_to_u32_rows(g["c2_head_out"].reshape(-1, 1)).reshape(8, 64, 2)).all()
+    assert (_u32(packed) == P.pack_u32(imgs.cpu().numpy())).all()
+    # K1 on the packed side output gives the same edges
+    assert (_u32(cu.edges_packed(packed, 64, 1)) == o).all()
+
+
+def torch_empty_like_words(imgs):
+    import torch
+
+    n, h, w = imgs.shape
+    return torch.empty((n, h, -(-w // 32)), dtype=torch.int32, device=imgs.device)
+
+
+def test_config_c3_full(cuda_dev):
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+
+    g = golden("configs.npz")
+    c3 = synth.c3_words()
+    out = _u32(cu.edges_packed(_t(c3.view(np.int32), cuda_dev), 8192, 1))
+    assert hashlib.sha256(out.tobytes()).digest() == g["c3_out_sha256"].tobytes()
+    # the same raster as the reference's native u64 words
+    w64 = _t(P.u32_rows_to_u64(c3).view(np.int64), cuda_dev)
+    o64 = _u64(cu.edges_packed(w64, 8192, 1))
+    assert (P.u64_to_u32_rows(o64) == out).all()
+
+
+@pytest.mark.slow
+def test_config_c4_full(cuda_dev):
+    """65536^2 (4 Gpx, 512 MiB packed): kernel vs the C per-pixel scanner, full size."""
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+
+    disks = synth.c4_disks()
+    slab = synth.c4_slab(0, synth.C4_SIZE, disks, device=cuda_dev)
+    out = cu.edges_packed(slab, synth.C4_SIZE, 1)
+    host_in = _u32(slab)
+    black = np.unpackbits(host_in[:2048].view(np.uint8)).mean()
+    assert 0.7 < black < 0.9            # ~19% black in the sample
+    exp = cscan.scan_p32(host_in, synth.C4_SIZE, 1)
+    assert (_u32(out) == exp).all()
+    # size-independent property: edges subset of figure (black out => black in)
+    assert not (~_u32(out) & host_in).any()
+
+
+@pytest.mark.slow
+def test_config_c5_sample(cuda_dev):
+    """Pages of the 1024 x 2048^2 batch vs the C scanner (64-page sample), plus
+    properties over a 256-page slice."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+
+    pages = synth.c5_pages(256, device=cuda_dev)
+    out = cu.pack_edges_u8(pages, 1)
+    host = pages[:64].cpu().numpy()
+    assert (_u32(out[:64]) == cscan.scan_u8(host, 1)).all()
+    # properties on all 256: edge subset of figure, and mask == per-pixel scan kernel
+    packed = cu.pack_u8(pages)
+    assert torch.equal(cu.edges_packed(packed, 2048, 1), out)
+    assert torch.equal(cu.scan_edges(packed, 2048, 1), out)
+    assert int(((~out) & packed).count_nonzero()) == 0
+
+
+# ---------------------------------------------------------------- row sharding (K3)
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_row_slabs_with_halos_equal_whole(cuda_dev, G):
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(G)
+    H, W = 301, 2048 + 96
+    a = (rng.random((H, W)) < 0.5).astype(np.uint8)
+    whole = cu.pack_edges_u8(_t(a, cuda_dev), 1)
+    pk = torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev)
+    edges = np.linspace(0, H, G + 1).astype(int)
+    for fill in (1, 0):
+        whole = cu.pack_edges_u8(_t(a, cuda_dev), fill)
+        parts = []
+        for r in range(G):
+            lo, hi = edges[r], edges[r + 1]
+            slab = pk[lo:hi].clone()
+            above = pk[lo - 1].clone() if lo > 0 else None
+            below = pk[hi].clone() if hi < H else None
+            out = torch.empty_like(slab)
+            # interior first, then the two boundary rows (the overlapped schedule)
+            if hi - lo > 2:
+                cu.edges_halo(slab, None, None, W, fill, out=out, row_lo=1, row_hi=hi - lo - 1)
+            cu.edges_halo(slab, above, below, W, fill, out=out, row_lo=0, row_hi=1)
+            cu.edges_halo(slab, above, below, W, fill, out=out, row_lo=hi - lo - 1, row_hi=hi - lo)
+            parts.append(out)
+        assert torch.equal(torch.cat(parts), whole), (G, fill)
+
+
+def test_host_pipeline_e2e(cuda_dev):
+    from paper_1401_5245_b200 import synth
+    from paper_1401_5245_b200.host import HostBatchEdges
+
+    imgs = synth.c2_images(512)
+    pipe = HostBatchEdges(imgs.shape, kind="u8", chunk_images=100)
+    hin, hout = pipe.new_host_buffers()
+    hin.copy_(imgs)
+    pipe(hin, hout)
+    assert (hout.numpy().view(np.uint32) == cscan.scan_u8(imgs.numpy(), 1)).all()
+    c3 = synth.c3_words(h=512)
+    pipe2 = HostBatchEdges((1, 512, 256), kind="packed", width=8192, chunk_images=1)
+    import torch
+
+    hin2 = torch.from_numpy(c3.view(np.int32)).reshape(1, 512, 256).pin_memory()
+    out2 = pipe2(hin2)
+    assert (out2.numpy().view(np.uint32)[0] == cscan.scan_p32(c3, 8192)).all()
+
+
+def test_fill_policies_on_border_touching_figure(cuda_dev):
+    """Interior invariance: pixels >= 2 from the border do not depend
+    on the policy; border pixels do."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    a = np.zeros((1, 20, 70), np.uint8)
+    a[0, 5:9, 30:40] = 1
+    t = _t(a, cuda_dev)
+    w = P.unpack_u32(_u32(cu.pack_edges_u8(t, 1)), 70)[0]
+    b = P.unpack_u32(_u32(cu.pack_edges_u8(t, 0)), 70)[0]
+    assert (w[2:-2, 2:-2] == b[2:-2, 2:-2]).all()
+    assert (w[0] == 0).all() and (b[0] == 1).all()
