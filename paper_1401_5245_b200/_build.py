@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbitedge_cuda.so")
 SOURCES = ["bitedge_capi.cu"]
-HEADERS = ["edge_tile.cuh", os.path.join("..", "..", "include", "bitedge.h")]
+HEADERS = ["edge_tile.cuh", "edge_stream.cuh", "edge_reg.cuh", os.path.join("..", "..", "include", "bitedge.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -9,10 +9,13 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/bitedge.h"
 #include "edge_tile.cuh"
+#include "edge_stream.cuh"
+#include "edge_reg.cuh"
 
 using namespace bitedge;
 
@@ -99,8 +102,257 @@ int launch_tile(TileParams &tp, int64_t rows, cudaStream_t st) {
     const int64_t grid = tiles_y * tp.tiles_x;
     if (grid <= 0) return BE_OK;
     if (grid > 0x7FFFFFFFLL) return fail(BE_EINVAL, "raster too large for one launch");
-    edge_tile_kernel<KIND><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    const bool others = tp.o_side[0] || tp.o_side[1] || tp.o_side[2] || tp.o_side[3] || tp.o_packed;
+    if (!others && tp.o_edges && !tp.o_eset)
+        edge_tile_kernel<KIND, kOutEdges><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    else if (!others && tp.o_eset && !tp.o_edges)
+        edge_tile_kernel<KIND, kOutEset><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    else
+        edge_tile_kernel<KIND, kOutAny><<<(unsigned)grid, kThreads, smem, st>>>(tp);
     return cuda_check("edge_tile_kernel");
+}
+
+// ---------------------------------------------------------------- streaming kernel
+
+int sm_count() {
+    thread_local int dev_cached = -1, sms_cached = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms_cached = v > 0 ? v : 148;
+        dev_cached = dev;
+    }
+    return sms_cached;
+}
+
+// Kernel selection knob for A/B measurements: BITEDGE_KERNEL=tile forces the
+// one-shot tile kernel, =stream forbids nothing (default: stream when eligible).
+bool stream_allowed() {
+    const char *e = getenv("BITEDGE_KERNEL");
+    return !(e && strcmp(e, "tile") == 0);
+}
+
+template <int KIND, int OUT>
+int launch_stream_out(StreamParams &sp, size_t smem, cudaStream_t st) {
+    thread_local size_t attr_set = 0;
+    if (smem > 48 * 1024 && smem > attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(edge_stream_kernel<KIND, OUT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail((int)e, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        attr_set = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_stream_kernel<KIND, OUT>, kThreads,
+                                                  smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > sp.ntiles) grid = sp.ntiles;
+    edge_stream_kernel<KIND, OUT><<<(unsigned)grid, kThreads, smem, st>>>(sp);
+    return cuda_check("edge_stream_kernel");
+}
+
+template <int KIND>
+int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
+    if (sp.o_edges && sp.o_eset) return launch_stream_out<KIND, kOutAny>(sp, smem, st);
+    if (sp.o_eset) return launch_stream_out<KIND, kOutEset>(sp, smem, st);
+    return launch_stream_out<KIND, kOutEdges>(sp, smem, st);
+}
+
+// ---------------------------------------------------------------- register-direct kernel
+
+// Launch helpers: dispatch the runtime choices onto template parameters.
+template <int OUT, bool HALO>
+int launch_reg_packed(RegParams &rp, int swap, int cw, unsigned grid, cudaStream_t st) {
+    if (swap) {
+        if (cw == 8) edge_reg_packed_kernel<1, 4, 8, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+        else edge_reg_packed_kernel<1, 4, 4, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+    } else {
+        if (cw == 8) edge_reg_packed_kernel<0, 4, 8, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+        else edge_reg_packed_kernel<0, 4, 4, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+    }
+    return cuda_check("edge_reg_packed_kernel");
+}
+
+template <int OUT, bool HALO>
+int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
+    if (rp.v8) {
+        if (rs == 8) edge_reg_u8_kernel<8, OUT, HALO, true><<<grid, kThreads, 0, st>>>(rp);
+        else edge_reg_u8_kernel<4, OUT, HALO, true><<<grid, kThreads, 0, st>>>(rp);
+    } else {
+        if (rs == 8) edge_reg_u8_kernel<8, OUT, HALO, false><<<grid, kThreads, 0, st>>>(rp);
+        else edge_reg_u8_kernel<4, OUT, HALO, false><<<grid, kThreads, 0, st>>>(rp);
+    }
+    return cuda_check("edge_reg_u8_kernel");
+}
+
+template <bool HALO>
+int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
+                    cudaStream_t st) {
+    if (input_kind == 1) {
+        if (rp.o_edges && rp.o_eset) return launch_reg_u8<kOutAny, HALO>(rp, rs, grid, st);
+        if (rp.o_eset) return launch_reg_u8<kOutEset, HALO>(rp, rs, grid, st);
+        return launch_reg_u8<kOutEdges, HALO>(rp, rs, grid, st);
+    }
+    if (rp.o_edges && rp.o_eset) return launch_reg_packed<kOutAny, HALO>(rp, swap, cw, grid, st);
+    if (rp.o_eset) return launch_reg_packed<kOutEset, HALO>(rp, swap, cw, grid, st);
+    return launch_reg_packed<kOutEdges, HALO>(rp, swap, cw, grid, st);
+}
+
+// Returns 1 when the register-direct kernel does not apply (caller falls back).
+int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
+            const void *below, uint32_t *o_edges, uint32_t *o_eset, int64_t out_stride_u32,
+            const Geometry &G, int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
+    const char *e = getenv("BITEDGE_KERNEL");
+    if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return 1;
+    auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
+    if (G.h >= ((int64_t)1 << 31)) return 1;
+    RegParams rp;
+    memset(&rp, 0, sizeof(rp));
+    rp.in = (const char *)in; rp.above = (const char *)above; rp.below = (const char *)below;
+    rp.in_row_bytes = in_row_bytes;
+    rp.o_edges = o_edges; rp.o_eset = o_eset; rp.out_stride = out_stride_u32;
+    rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
+    rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
+    rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
+    auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+    const bool in32 = al(in, 32) && in_row_bytes % 32 == 0 && al(above, 32) && al(below, 32);
+    // packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4
+    // (only when that still gives >= 4 waves of threads; small rasters want more threads)
+    const int64_t strips4 = (row_hi - row_lo + 3) / 4;
+    const int cw = (input_kind == 0 && in32 && !getenv("BITEDGE_CW4") &&
+                    strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096)
+                       ? 8
+                       : 4;
+    rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
+    rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
+    const int ocw = input_kind == 1 ? 1 : cw;
+    rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
+    if (input_kind == 1 && !above && !below && row_lo == 0 && row_hi == nrows &&
+        in_row_bytes == G.w && ((uintptr_t)in % 32) == 0 && G.w % 32 == 0 && G.wp <= 32 &&
+        (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !getenv("BITEDGE_NO_WARPIMG")) {
+        const int lwpr = ilog2(G.wp), rpi = 32 >> lwpr;
+        if (G.h % rpi == 0 && G.h / rpi <= 8) {
+            const int groups = (int)(G.h / rpi);
+            const int64_t nimg = G.n;
+            const int64_t grid = (nimg * 32 + kThreads - 1) / kThreads;
+            if (grid <= 0x7FFFFFFFLL) {
+#define BE_WARPIMG(L)                                                                          \
+    case L:                                                                                    \
+        if (o_edges && o_eset)                                                                 \
+            edge_warp_img_kernel<L, kOutAny><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+        else if (o_eset)                                                                       \
+            edge_warp_img_kernel<L, kOutEset><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+        else                                                                                   \
+            edge_warp_img_kernel<L, kOutEdges><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+        return cuda_check("edge_warp_img_kernel");
+                switch (lwpr) {
+                    BE_WARPIMG(0)
+                    BE_WARPIMG(1)
+                    BE_WARPIMG(2)
+                    BE_WARPIMG(3)
+                    BE_WARPIMG(4)
+                    BE_WARPIMG(5)
+                    default: break;
+                }
+#undef BE_WARPIMG
+            }
+        }
+    }
+    const int64_t rows = row_hi - row_lo;
+    // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
+    constexpr int kRSL = 32;
+    if (input_kind == 1 && rp.v8 && !getenv("BITEDGE_NO_ROLL") &&
+        (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
+        rp.nstrips = (rows + kRSL - 1) / kRSL;
+        const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
+        if (g <= 0x7FFFFFFFLL) {
+            const unsigned grid = (unsigned)g;
+            const bool halo = above || below;
+            if (rp.o_edges && rp.o_eset) {
+                if (halo) edge_roll_u8_kernel<kRSL, kOutAny, true><<<grid, kThreads, 0, st>>>(rp);
+                else edge_roll_u8_kernel<kRSL, kOutAny, false><<<grid, kThreads, 0, st>>>(rp);
+            } else if (rp.o_eset) {
+                if (halo) edge_roll_u8_kernel<kRSL, kOutEset, true><<<grid, kThreads, 0, st>>>(rp);
+                else edge_roll_u8_kernel<kRSL, kOutEset, false><<<grid, kThreads, 0, st>>>(rp);
+            } else {
+                if (halo) edge_roll_u8_kernel<kRSL, kOutEdges, true><<<grid, kThreads, 0, st>>>(rp);
+                else edge_roll_u8_kernel<kRSL, kOutEdges, false><<<grid, kThreads, 0, st>>>(rp);
+            }
+            return cuda_check("edge_roll_u8_kernel");
+        }
+    }
+    // strip height: 4 rows (the one-shot kernels keep every row of the strip in flight)
+    int rs = 4;
+    if (input_kind == 1) {
+        const char *rse = getenv("BITEDGE_RS");
+        if (rse) rs = atoi(rse) == 8 ? 8 : 4;
+    }
+    rp.nstrips = (rows + rs - 1) / rs;
+    const int64_t threads = rp.nstrips * rp.items;
+    const int64_t grid = (threads + kThreads - 1) / kThreads;
+    if (grid > 0x7FFFFFFFLL) return 1;
+    if (above || below)
+        return launch_reg_halo<true>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
+    return launch_reg_halo<false>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
+}
+
+// Returns 1 when the streaming kernel does not apply (caller falls back).
+int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
+               const void *below, uint32_t *o_edges, uint32_t *o_eset, int word_bits,
+               int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
+               int64_t row_hi, cudaStream_t st) {
+    if (!stream_allowed()) return 1;
+    auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
+    if (nrows >= ((int64_t)1 << 31)) return 1;                     // 32-bit row arithmetic
+    StreamParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.in = (const char *)in; sp.above = (const char *)above; sp.below = (const char *)below;
+    sp.in_row_bytes = in_row_bytes;
+    sp.o_edges = o_edges; sp.o_eset = o_eset; sp.out_stride = out_stride_u32;
+    sp.nrows = nrows; sp.h = G.h; sp.w = G.w; sp.row_lo = row_lo; sp.row_hi = row_hi;
+    sp.wp = G.wp; sp.pl = G.pl; sp.lastbit = G.lastbit; sp.padmask = G.padmask;
+    sp.fillword = G.fillword;
+    sp.vst = (out_stride_u32 % 4 == 0) && al16(o_edges) && al16(o_eset);
+    int TQ, stage_target = 24 * 1024;
+    if (input_kind == 0) {
+        const int64_t wpr = (G.wp + 3) / 4 * 4;                 // words readable per row
+        TQ = wpr >= 256 ? 256 : next_pow2(wpr);
+        sp.tiles_x = (G.wp + TQ - 1) / TQ;
+        sp.contiguous = sp.tiles_x == 1 && in_row_bytes <= 8 * wpr;
+        sp.raw_pitch = sp.contiguous ? (int)in_row_bytes : 4 * TQ + 32;
+        sp.col0 = sp.contiguous ? 0 : 16;
+        sp.row_bytes_alloc = sp.contiguous ? in_row_bytes : 4 * wpr;
+    } else {
+        TQ = G.wp >= 64 ? 64 : next_pow2(G.wp);
+        sp.tiles_x = (G.wp + TQ - 1) / TQ;
+        const int64_t wr = (G.w + 15) / 16 * 16;
+        sp.contiguous = sp.tiles_x == 1 && in_row_bytes <= 2 * wr;
+        sp.raw_pitch = sp.contiguous ? (int)in_row_bytes : 32 * TQ + 32;
+        sp.col0 = sp.contiguous ? 0 : 16;
+        sp.row_bytes_alloc = sp.contiguous ? in_row_bytes : wr;
+        const int room = (sp.raw_pitch - sp.col0) / 16;
+        sp.pieces = room < 2 * TQ ? room : 2 * TQ;
+    }
+    if (sp.raw_pitch > stage_target / 3) return 1;                 // rows too wide to stage
+    sp.log_tq = ilog2(TQ);
+    int R = stage_target / sp.raw_pitch - 2;
+    const int64_t rows = row_hi - row_lo;
+    if (R > rows) R = (int)rows;
+    if (R < 1) R = 1;
+    sp.R = R;
+    sp.ntiles = ((rows + R - 1) / R) * sp.tiles_x;
+    sp.stage_bytes = ((R + 2) * sp.raw_pitch + 127) / 128 * 128;
+    sp.stages = 4;
+    size_t smem = (size_t)sp.stages * sp.stage_bytes + 8 * sp.stages;
+    if (input_kind == 1) smem += (size_t)(R + 2) * (TQ + 8) * 4;
+    if (smem > 110 * 1024) return 1;
+    if (input_kind == 1) return launch_stream_kind<kSU8>(sp, smem, st);
+    return word_bits == 64 ? launch_stream_kind<kSP64>(sp, smem, st)
+                           : launch_stream_kind<kSP32>(sp, smem, st);
 }
 
 // Shared driver of every fused-edge entry point.
@@ -160,21 +412,39 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     tp.tiles_x = (G.wp + TQ - 1) / TQ;
 
     cudaStream_t st = S(stream);
+    const bool only_edges = !o_side[0] && !o_side[1] && !o_side[2] && !o_side[3] && !o_packed;
     if (input_kind == 0) {
         if ((rc = check_ptr(in, word_bits, "input"))) return rc;
         if ((rc = check_stride(G, in_stride, "input"))) return rc;
         if (above && (rc = check_ptr(above, word_bits, "above halo"))) return rc;
         if (below && (rc = check_ptr(below, word_bits, "below halo"))) return rc;
         tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
+        if (only_edges) {
+            rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
+                         tp.out_stride, G, nrows, row_lo, row_hi, st);
+            if (rc != 1) return rc;
+            rc = try_stream(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
+                            word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st);
+            if (rc != 1) return rc;
+        }
         bool vec = TQ >= 4 && (tp.in_stride % 4) == 0 && ((uintptr_t)in % 16) == 0 &&
                    (!above || ((uintptr_t)above % 16) == 0) &&
                    (!below || ((uintptr_t)below % 16) == 0);
-        return vec ? launch_tile<kPackedVec>(tp, rows, st)
-                   : launch_tile<kPackedScalar>(tp, rows, st);
+        if (!vec) return launch_tile<kPScalar>(tp, rows, st);
+        return word_bits == 64 ? launch_tile<kP64Vec>(tp, rows, st)
+                               : launch_tile<kP32Vec>(tp, rows, st);
     }
     if (in_stride < w) return fail(BE_EINVAL, "input row stride %lld bytes < width %lld",
                                    (long long)in_stride, (long long)w);
     tp.in_stride = in_stride;
+    if (only_edges && word_bits == 32) {
+        rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, tp.out_stride, G, nrows,
+                     row_lo, row_hi, st);
+        if (rc != 1) return rc;
+        rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
+                        G, nrows, row_lo, row_hi, st);
+        if (rc != 1) return rc;
+    }
     bool vec = (in_stride % 16) == 0 && ((uintptr_t)in % 16) == 0 &&
                (!above || ((uintptr_t)above % 16) == 0) && (!below || ((uintptr_t)below % 16) == 0);
     return vec ? launch_tile<kU8Vec>(tp, rows, st) : launch_tile<kU8Byte>(tp, rows, st);

@@ -32,10 +32,17 @@ namespace bitedge {
 constexpr int kThreads = 256;
 
 enum LoadKind : int {
-    kPackedVec = 0,    // packed words, 128-bit loads (16-B aligned rows)
-    kPackedScalar = 1, // packed words, 32-bit loads
-    kU8Vec = 2,        // uint8 pixels, 128-bit loads
-    kU8Byte = 3,       // uint8 pixels, byte loads (unaligned rows)
+    kP32Vec = 0,       // uint32 row words, 128-bit loads (16-B aligned rows)
+    kP64Vec = 1,       // uint64 row words, 128-bit loads, halves swapped into pixel order
+    kPScalar = 2,      // packed words of either format, 32-bit loads
+    kU8Vec = 3,        // uint8 pixels, 128-bit loads
+    kU8Byte = 4,       // uint8 pixels, byte loads (unaligned rows)
+};
+
+enum OutKind : int {
+    kOutEdges = 0,     // detect_edges_mask only (the hot path)
+    kOutEset = 1,      // EdgeSet only
+    kOutAny = 2,       // any subset of the optional outputs
 };
 
 struct TileParams {
@@ -104,165 +111,154 @@ __device__ __forceinline__ uint32_t pack16_bytes(const uint8_t *row, int64_t x0,
     return v;
 }
 
+
+// Pointer to global row g of the staged range, or nullptr when that row does
+// not exist (outside the raster with no halo buffer).
 template <int KIND>
-__device__ __forceinline__ const void *row_ptr(const TileParams &p, int64_t g) {
-    const int64_t elem = (KIND == kU8Vec || KIND == kU8Byte) ? 1 : 4;
-    if (g >= 0 && g < p.nrows)
-        return (const char *)p.in + g * p.in_stride * elem;
-    if (g == -1) return p.above;
-    if (g == p.nrows) return p.below;
+__device__ __forceinline__ const char *row_ptr(const TileParams &p, int64_t g) {
+    constexpr int64_t elem = (KIND == kU8Vec || KIND == kU8Byte) ? 1 : 4;
+    if (g >= 0 && g < p.nrows) return (const char *)p.in + g * p.in_stride * elem;
+    if (g == -1) return (const char *)p.above;
+    if (g == p.nrows) return (const char *)p.below;
     return nullptr;
 }
 
+// Stage one 4-word chunk / 16-pixel piece of a row into shared memory.
 template <int KIND>
+__device__ __forceinline__ void stage_item(uint32_t *srow, const char *row, int c, int pw0,
+                                           int64_t x0, const TileParams &p) {
+    if (KIND == kP32Vec || KIND == kP64Vec) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (row != nullptr && pw0 < p.wp) v = ldg_stream_v4((const uint32_t *)row + pw0);
+        if (KIND == kP64Vec) v = make_uint4(v.y, v.x, v.w, v.z);
+        *reinterpret_cast<uint4 *>(srow + 4 * c) = v;
+    } else if (KIND == kPScalar) {
+        uint32_t v = 0u;
+        if (row != nullptr && pw0 < p.wp) v = ldg_u32((const uint32_t *)row + (pw0 ^ p.swap));
+        srow[c] = v;
+    } else {
+        uint32_t half = 0xFFFFu;
+        if (row != nullptr && x0 < p.w) {
+            if (KIND == kU8Vec && x0 + 16 <= p.w) half = pack16(ldg_stream_v4(row + x0));
+            else half = pack16_bytes((const uint8_t *)row, x0, p.w);
+        }
+        reinterpret_cast<uint16_t *>(srow)[2 * (c >> 1) + ((c & 1) ? 0 : 1)] = (uint16_t)half;
+    }
+}
+
+template <int KIND, int OUT>
 __global__ void __launch_bounds__(kThreads)
 edge_tile_kernel(const TileParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    const int TQ = 1 << p.log_tq;
+    constexpr bool U8 = (KIND == kU8Vec || KIND == kU8Byte);
+    const int log_tq = p.log_tq;
+    const int TQ = 1 << log_tq;
     const int R = 1 << p.log_r;
     const int P = TQ + 8;                    // row pitch; interior starts at column 4
     uint8_t *flags = reinterpret_cast<uint8_t *>(smem + (R + 2) * P);
     const int tid = threadIdx.x;
 
-    const int64_t tile = blockIdx.x;
-    const int tx = (int)(tile % p.tiles_x);
-    const int64_t g0 = p.row_lo + (tile / p.tiles_x) * (int64_t)R;
+    const int tx = (int)(blockIdx.x % (unsigned)p.tiles_x);
+    const int64_t g0 = p.row_lo + (int64_t)(blockIdx.x / (unsigned)p.tiles_x) * R;
     const int q0 = tx * TQ;
 
-    // ---- stage rows g0-1 .. g0+R into shared memory as pixel-order words ----
-    // Halo words left (q0-1) and right (q0+TQ) of every staged row.  They exist
-    // only when a row spans several column tiles (then TQ = 64 and R <= 64, so
-    // one item per thread); otherwise both lie outside the row and hold the fill.
-    const bool multi_col = p.tiles_x > 1;
-    uint32_t halo_v = p.fillword;
-    if (multi_col && tid < 2 * (R + 2)) {
+    // ---- stage rows g0-1 .. g0+R (smem rows 0 .. R+1) as pixel-order words ----
+    // Items per staged row: 4-word chunks (packed, vector), words (scalar) or
+    // 16-pixel pieces (uint8).  The item count divides the thread count, so a
+    // thread keeps the same column item for every row it stages.
+    const int log_items = (KIND == kP32Vec || KIND == kP64Vec) ? log_tq - 2
+                          : (U8 ? log_tq + 1 : log_tq);
+    const int items = 1 << log_items;
+    const int c = tid & (items - 1);
+    const int rstep = kThreads >> log_items;          // staged rows per pass
+    const int pw0 = (KIND == kP32Vec || KIND == kP64Vec) ? q0 + 4 * c : q0 + c;
+    const int64_t x0 = (int64_t)q0 * 32 + 16 * c;     // uint8: first pixel of the piece
+    {
+        // main rows (smem 1..R): global rows g0 .. g0+R-1, all inside `in`
+        const int nvalid = (int)min((int64_t)R, p.nrows - g0);
+        const int64_t rs = p.in_stride * (U8 ? 1 : 4);             // bytes per row
+        const char *base = (const char *)p.in + g0 * rs;
+        constexpr int U = 4;
+        for (int r0 = tid >> log_items; r0 < R; r0 += U * rstep) {
+            if (KIND == kP32Vec || KIND == kP64Vec || KIND == kU8Vec) {
+                // issue up to U independent 16-byte loads before consuming any
+                uint4 v[U];
+                bool full[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u * rstep;
+                    full[u] = false;
+                    v[u] = make_uint4(0u, 0u, 0u, 0u);
+                    if (r < nvalid) {
+                        const char *row = base + r * rs;
+                        if (U8) {
+                            if (x0 + 16 <= p.w) { v[u] = ldg_stream_v4(row + x0); full[u] = true; }
+                        } else if (pw0 < p.wp) {
+                            v[u] = ldg_stream_v4((const uint32_t *)row + pw0);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u * rstep;
+                    if (r < R) {
+                        uint32_t *srow = smem + (r + 1) * P + 4;
+                        if (U8) {
+                            uint32_t half = 0xFFFFu;
+                            if (full[u]) half = pack16(v[u]);
+                            else if (r < nvalid && x0 < p.w)
+                                half = pack16_bytes((const uint8_t *)(base + r * rs), x0, p.w);
+                            reinterpret_cast<uint16_t *>(srow)[2 * (c >> 1) + ((c & 1) ? 0 : 1)] =
+                                (uint16_t)half;
+                        } else {
+                            uint4 x = v[u];
+                            if (KIND == kP64Vec) x = make_uint4(x.y, x.x, x.w, x.z);
+                            *reinterpret_cast<uint4 *>(srow + 4 * c) = x;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u * rstep;
+                    if (r < R)
+                        stage_item<KIND>(smem + (r + 1) * P + 4, r < nvalid ? base + r * rs : nullptr,
+                                         c, pw0, x0, p);
+                }
+            }
+        }
+        // halo rows: smem 0 = global g0-1, smem R+1 = global g0+R
+        if (tid < 2 * items) {
+            const int side = tid >> log_items;
+            const int64_t g = side ? g0 + R : g0 - 1;
+            stage_item<KIND>(smem + (side ? R + 1 : 0) * P + 4, row_ptr<KIND>(p, g), c, pw0, x0, p);
+        }
+    }
+    // Column halo words (q0-1, q0+TQ) exist only when a row spans several
+    // column tiles (then TQ = 64 and R <= 64: one item per thread); otherwise
+    // they lie outside the row and hold the fill.
+    if (tid < 2 * (R + 2)) {
         const int i = tid >> 1, right = tid & 1;
         const int pw = right ? q0 + TQ : q0 - 1;
-        if (pw >= 0 && pw < p.wp) {
-            if (KIND == kPackedVec || KIND == kPackedScalar) {
-                const uint32_t *row = (const uint32_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                if (row != nullptr) halo_v = ldg_u32(row + (pw ^ p.swap));
-            } else {
-                // only the pixel adjacent to the tile matters: load that 16-pixel piece
-                const uint8_t *row = (const uint8_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                const int64_t x0 = (int64_t)pw * 32 + (right ? 0 : 16);
-                if (row != nullptr && x0 < p.w) {
-                    const uint32_t half = pack16_bytes(row, x0, p.w);
-                    halo_v = right ? (half << 16) : half;
+        uint32_t v = p.fillword;
+        if (p.tiles_x > 1 && pw >= 0 && pw < p.wp) {
+            const char *row = row_ptr<KIND>(p, g0 - 1 + i);
+            if (row != nullptr) {
+                if (!U8) {
+                    v = ldg_u32((const uint32_t *)row + (pw ^ p.swap));
+                } else {
+                    const int64_t hx = (int64_t)pw * 32 + (right ? 0 : 16);
+                    if (hx < p.w) {
+                        const uint32_t half = pack16_bytes((const uint8_t *)row, hx, p.w);
+                        v = right ? (half << 16) : half;
+                    }
                 }
             }
         }
-    }
-    // Interior: batches of U loads are issued back to back before any result is
-    // consumed, so every thread keeps U 16-byte requests in flight.
-    constexpr int U = 8;
-    if (KIND == kPackedVec) {
-        const int log_ch = p.log_tq - 2;
-        const int CH = 1 << log_ch;
-        const int total = (R + 2) * CH;
-        for (int base = tid; base < total; base += U * kThreads) {
-            uint4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int idx = base + u * kThreads;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (idx < total) {
-                    const int i = idx >> log_ch, pw = q0 + 4 * (idx & (CH - 1));
-                    const uint32_t *row = (const uint32_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                    if (row != nullptr && pw < p.wp) v[u] = ldg_stream_v4(row + pw);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int idx = base + u * kThreads;
-                if (idx < total) {
-                    const int i = idx >> log_ch, c = idx & (CH - 1);
-                    uint4 x = v[u];
-                    if (p.swap) x = make_uint4(x.y, x.x, x.w, x.z);
-                    *reinterpret_cast<uint4 *>(smem + i * P + 4 + 4 * c) = x;
-                }
-            }
-        }
-    } else if (KIND == kPackedScalar) {
-        const int total = (R + 2) * TQ;
-        for (int base = tid; base < total; base += U * kThreads) {
-            uint32_t v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int idx = base + u * kThreads;
-                v[u] = 0u;
-                if (idx < total) {
-                    const int i = idx >> p.log_tq, pw = q0 + (idx & (TQ - 1));
-                    const uint32_t *row = (const uint32_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                    if (row != nullptr && pw < p.wp) v[u] = ldg_u32(row + (pw ^ p.swap));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int idx = base + u * kThreads;
-                if (idx < total) smem[(idx >> p.log_tq) * P + 4 + (idx & (TQ - 1))] = v[u];
-            }
-        }
+        smem[i * P + 4 + (right ? TQ : -1)] = v;
     } else {
-        // uint8 pixels: piece k of a tile row = 16 pixels = one half of word k/2;
-        // a word's high half (u16 index 2*word+1) holds its left 16 pixels.
-        uint16_t *sm16 = reinterpret_cast<uint16_t *>(smem);
-        const int log_npc = p.log_tq + 1;
-        const int NPC = 1 << log_npc;
-        const int total = (R + 2) * NPC;
-        if (KIND == kU8Vec) {
-            for (int base = tid; base < total; base += U * kThreads) {
-                uint4 v[U];
-                uint32_t st[U];   // 0: vector piece, 1: partial (byte path), 2: outside
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int idx = base + u * kThreads;
-                    st[u] = 2;
-                    if (idx < total) {
-                        const int i = idx >> log_npc, k = idx & (NPC - 1);
-                        const int64_t x0 = (int64_t)(q0 + (k >> 1)) * 32 + (k & 1) * 16;
-                        const uint8_t *row = (const uint8_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                        if (row != nullptr && x0 < p.w) {
-                            if (x0 + 16 <= p.w) {
-                                v[u] = ldg_stream_v4(row + x0);
-                                st[u] = 0;
-                            } else {
-                                st[u] = 1;
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int idx = base + u * kThreads;
-                    if (idx < total) {
-                        const int i = idx >> log_npc, k = idx & (NPC - 1);
-                        uint32_t half = 0xFFFFu;
-                        if (st[u] == 0) {
-                            half = pack16(v[u]);
-                        } else if (st[u] == 1) {
-                            const int64_t x0 = (int64_t)(q0 + (k >> 1)) * 32 + (k & 1) * 16;
-                            half = pack16_bytes((const uint8_t *)row_ptr<KIND>(p, g0 - 1 + i),
-                                                x0, p.w);
-                        }
-                        sm16[2 * (i * P + 4 + (k >> 1)) + ((k & 1) ? 0 : 1)] = (uint16_t)half;
-                    }
-                }
-            }
-        } else {
-            for (int idx = tid; idx < total; idx += kThreads) {
-                const int i = idx >> log_npc, k = idx & (NPC - 1);
-                const int64_t x0 = (int64_t)(q0 + (k >> 1)) * 32 + (k & 1) * 16;
-                const uint8_t *row = (const uint8_t *)row_ptr<KIND>(p, g0 - 1 + i);
-                uint32_t half = 0xFFFFu;
-                if (row != nullptr && x0 < p.w) half = pack16_bytes(row, x0, p.w);
-                sm16[2 * (i * P + 4 + (k >> 1)) + ((k & 1) ? 0 : 1)] = (uint16_t)half;
-            }
-        }
-    }
-    for (int idx = tid; idx < 2 * (R + 2); idx += kThreads) {
-        const int i = idx >> 1, right = idx & 1;
-        smem[i * P + 4 + (right ? TQ : -1)] = idx == tid ? halo_v : p.fillword;
+        for (int idx = tid; idx < 2 * (R + 2); idx += kThreads)
+            smem[(idx >> 1) * P + 4 + ((idx & 1) ? TQ : -1)] = p.fillword;
     }
     // per-row border flags: bit0 -> row above is outside the image, bit1 -> below
     for (int i = tid; i < R; i += kThreads) {
@@ -278,41 +274,49 @@ edge_tile_kernel(const TileParams p) {
     __syncthreads();
 
     // ---- one fused pass per output word ----
+    // Thread -> fixed word column j, rows r, r + NG, ...; every per-column
+    // quantity (border column, pixel w-1 fix, padding) is loop-invariant.
+    const int j = tid & (TQ - 1);
+    const int NG = kThreads >> log_tq;
+    const int pw = q0 + j;
+    if (pw >= p.wp) return;
     const uint32_t fw = p.fillword;
-    for (int idx = tid; idx < R * TQ; idx += kThreads) {
-        const int i = idx >> p.log_tq, j = idx & (TQ - 1);
-        const int64_t g = g0 + i;
-        if (g >= p.row_hi) break;
-        const int pw = q0 + j;
-        if (pw >= p.wp) continue;
-        const uint32_t *s = smem + (i + 1) * P + 4 + j;
-        const uint32_t c = s[0];
-        const uint32_t f = flags[i];
+    const bool first_col = (pw == 0);
+    uint32_t keep = 0xFFFFu | 0xFFFF0000u, fixb = 0u, force = 0u;
+    if (pw == p.pl) {
+        keep = ~p.lastbit;                 // pixel w-1 reads the fill (bitimage.py:234-239)
+        fixb = fw & p.lastbit;
+        force = p.padmask;
+    } else if (pw > p.pl) {
+        force = 0xFFFFFFFFu;               // all-padding word
+    }
+    const int rmax = (int)min((int64_t)R, p.row_hi - g0);
+    const int64_t ostep = (int64_t)NG * p.out_stride;
+    int64_t o = (g0 + (tid >> log_tq)) * p.out_stride + (pw ^ p.swap);
+    const uint32_t *s = smem + ((tid >> log_tq) + 1) * P + 4 + j;
+    const int sstep = NG * P;
+    for (int r = tid >> log_tq; r < rmax; r += NG, s += sstep, o += ostep) {
+        const uint32_t cc = s[0];
+        const uint32_t f = flags[r];
         const uint32_t u = (f & 1) ? fw : s[-P];
         const uint32_t d = (f & 2) ? fw : s[P];
-        const uint32_t l = (pw == 0) ? fw : s[-1];
-        const uint32_t r = s[1];
-        const uint32_t ln = __funnelshift_r(c, l, 1);   // (c >> 1) | (l << 31)
-        uint32_t rn = __funnelshift_l(r, c, 1);         // (c << 1) | (r >> 31)
-        uint32_t pad = 0u, dead = 0u;
-        if (pw >= p.pl) {
-            if (pw == p.pl) {
-                rn = (rn & ~p.lastbit) | (fw & p.lastbit);  // pixel w-1 reads the fill
-                pad = p.padmask;
-            } else {
-                dead = ~0u;                                  // all-padding word
-            }
-        }
+        const uint32_t l = first_col ? fw : s[-1];
+        const uint32_t ln = __funnelshift_r(cc, l, 1);           // (c >> 1) | (l << 31)
+        const uint32_t rn = (__funnelshift_l(s[1], cc, 1) & keep) | fixb;  // (c << 1) | (r >> 31)
         const uint32_t any = ln | rn | u | d;
-        const int64_t o = g * p.out_stride + (pw ^ p.swap);
-        const uint32_t force = pad | dead;
-        if (p.o_edges) p.o_edges[o] = c | ~any | force;
-        if (p.o_eset) p.o_eset[o] = (~c & any) | force;
-        if (p.o_side[0]) p.o_side[0][o] = (ln & ~c) | force;
-        if (p.o_side[1]) p.o_side[1][o] = (rn & ~c) | force;
-        if (p.o_side[2]) p.o_side[2][o] = (u & ~c) | force;
-        if (p.o_side[3]) p.o_side[3][o] = (d & ~c) | force;
-        if (p.o_packed) p.o_packed[o] = c | force;
+        if (OUT == kOutEdges) {
+            __stcs(p.o_edges + o, cc | ~any | force);
+        } else if (OUT == kOutEset) {
+            __stcs(p.o_eset + o, (~cc & any) | force);
+        } else {
+            if (p.o_edges) p.o_edges[o] = cc | ~any | force;
+            if (p.o_eset) p.o_eset[o] = (~cc & any) | force;
+            if (p.o_side[0]) p.o_side[0][o] = (ln & ~cc) | force;
+            if (p.o_side[1]) p.o_side[1][o] = (rn & ~cc) | force;
+            if (p.o_side[2]) p.o_side[2][o] = (u & ~cc) | force;
+            if (p.o_side[3]) p.o_side[3][o] = (d & ~cc) | force;
+            if (p.o_packed) p.o_packed[o] = cc | force;
+        }
     }
 }
 

@@ -117,9 +117,17 @@ def edges_packed(words: torch.Tensor, width: int, border=WHITE_OUTSIDE, *, out=N
     w3, wb, rs = _packed(words, width)
     o = _new_like(w3, squeeze) if out is None else out
     o3 = _check_out(o, w3, squeeze)
-    if _row_stride(o3, "out") != rs:
-        raise ValueError("out must have the input's row stride")
     n, h, _ = w3.shape
+    ors = _row_stride(o3, "out")
+    if ors != rs:   # different input / output strides: the general entry point
+        outs = _capi.be_outputs()
+        if edgeset:
+            outs.edgeset = o3.data_ptr()
+        else:
+            outs.edges = o3.data_ptr()
+        _capi.call("be_edges_general", _ptr(w3), 0, rs, None, None, ctypes.byref(outs), wb, ors,
+                   n, h, int(width), fill_bit(border), 0, n * h, ctypes.c_void_p(_stream(w3)))
+        return o
     name = "be_edge_packed_u64" if wb == 64 else "be_edge_packed_u32"
     _capi.call(name, _ptr(w3), _ptr(o3), n, h, int(width), rs, fill_bit(border), int(edgeset),
                ctypes.c_void_p(_stream(w3)))

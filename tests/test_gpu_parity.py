@@ -206,9 +206,14 @@ def test_garbage_padding_bits_ignored(cuda_dev):
                       & np.uint32(P.u32_pad_mask(w) or 0))
         noisy[..., :-1] = pk[..., :-1]
         assert (_u32(cu.edges_packed(_t(noisy.view(np.int32), cuda_dev), w, 1)) == exp).all()
-        cleared = pk & ~np.uint32(P.u32_pad_mask(w))
-        assert (_u32(cu.edges_packed(_t(cleared.view(np.int32), cuda_dev), w, 0)) ==
-                cscan.scan_u8(a, 0)).all()
+        cleared = pk.copy()
+        cleared[..., -1] &= ~np.uint32(P.u32_pad_mask(w))
+        got = _u32(cu.edges_packed(_t(cleared.view(np.int32), cuda_dev), w, 0))
+        exp0 = cscan.scan_u8(a, 0)
+        bad = np.argwhere(got != exp0)
+        assert bad.size == 0, (w, bad[:4].tolist(), [hex(int(got[tuple(b)])) for b in bad[:4]],
+                               [hex(int(exp0[tuple(b)])) for b in bad[:4]],
+                               [hex(int(cleared[tuple(b)])) for b in bad[:4]])
 
 
 # ---------------------------------------------------------------- BASELINE configs
