@@ -373,27 +373,56 @@ def run_ours(args):
         torch.cuda.current_stream(dev).wait_stream(s)
         torch.cuda.synchronize()
 
-        def capture(count):
+        def capture(count, nstreams):
+            """Graph of `count` consecutive steps; with nstreams > 1 the steps
+            (independent batches) alternate over parallel fork/join branches so
+            one batch's kernel can overlap the previous one's tail."""
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                for i in range(count):
-                    step(i)
+                if nstreams <= 1:
+                    for i in range(count):
+                        step(i)
+                else:
+                    cur = torch.cuda.current_stream(dev)
+                    side = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+                    for s_ in side:
+                        s_.wait_stream(cur)
+                    for i in range(count):
+                        with torch.cuda.stream(side[i % nstreams]):
+                            step(i)
+                    for s_ in side:
+                        cur.wait_stream(s_)
             return g
-        chunk = min(pool, max(1, steps))
-        g_full = capture(chunk)
+        chunk = min(max(1, steps), 1024)
+        g_full = capture(chunk, args.streams)
         rem = steps % chunk
-        g_rem = capture(rem) if rem else None
+        g_rem = capture(rem, args.streams) if rem else None
 
         def run(k):
             q, r = divmod(k, chunk)
             for _ in range(q):
                 g_full.replay()
             if r:
-                (g_rem if r == rem and g_rem is not None else capture(r)).replay()
+                (g_rem if r == rem and g_rem is not None else capture(r, args.streams)).replay()
+
+        def serial_step_ms():
+            """Single-stream (no overlap) time per step: the per-launch latency."""
+            n_s = min(max(steps, 8), 512)
+            gs = capture(n_s, 1)
+            gs.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            gs.replay()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n_s
     else:
         def run(k):
             for i in range(k):
                 step(i)
+
+        serial_step_ms = None
 
     # ---- warm-up, then exactly K timed steps (barrier + sync on both sides)
     run(warmup)
@@ -425,11 +454,11 @@ def run_ours(args):
     value = px_all * steps / (ms_max / 1e3) / 1e9
     ms_step = ms_max / steps
 
-    # ---- single-launch duration of the dominant kernel (cold L2 via pool rotation)
-    per_launch_ms = ms / steps / launches_per_step if launches_per_step == 1 else None
-    if per_launch_ms is None:
-        per_launch_ms = ms / steps
+    # ---- roofline of the dominant kernel: algorithmic bytes per launch over the
+    # average launch duration in the timed region (steps overlap when streams > 1)
+    per_launch_ms = ms / steps / launches_per_step
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    serial_ms = serial_step_ms() if (use_graph and args.streams > 1) else None
     peak, peak_src = measured_peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -494,12 +523,17 @@ def run_ours(args):
                                     f"({pool * step_bytes / 2**20:.0f} MiB > 3x L2 "
                                     f"{l2 / 2**20:.0f} MiB)" if pool > 1 else
                                     f"step footprint {step_bytes / 2**20:.0f} MiB > L2",
-                       "launch": "CUDA graph replay" if use_graph else "direct launches"},
+                       "launch": ("CUDA graph replay, independent batches on "
+                                  f"{args.streams} parallel branches") if use_graph
+                                 else "direct launches"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes,
                          "avg_launch_us": per_launch_ms * 1e3,
+                         "serial_launch_us": serial_ms * 1e3 if serial_ms else None,
+                         "frac_serial": (alg_bytes / (serial_ms / 1e3) / 1e9 / peak)
+                         if serial_ms else None,
                          "bytes_per_px": BYTES_PER_PX[kind]},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches),
             "clocks": clocks, "parity": parity,
@@ -545,6 +579,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="parallel graph branches for independent batches (1 = serial)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")

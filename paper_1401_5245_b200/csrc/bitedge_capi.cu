@@ -91,6 +91,30 @@ int check_ptr(const void *p, int word_bits, const char *what) {
     return BE_OK;
 }
 
+// Launch with programmatic dependent launch enabled (BITEDGE_PDL=0 disables): the
+// kernel's CTAs may be scheduled while the previous kernel on the stream drains;
+// they block in griddepcontrol.wait until its results are visible.
+bool pdl_enabled() {
+    const char *e = getenv("BITEDGE_PDL");
+    return !(e && e[0] == '0');
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(bitedge::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 inline int ilog2(int v) { int l = 0; while ((1 << (l + 1)) <= v) ++l; return l; }
 inline int next_pow2(int64_t v) { int p = 1; while (p < v && p < (1 << 30)) p <<= 1; return p; }
 
@@ -166,11 +190,11 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, unsigned grid, cudaStream_t st) {
     if (swap) {
-        if (cw == 8) edge_reg_packed_kernel<1, 4, 8, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
-        else edge_reg_packed_kernel<1, 4, 4, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+        if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
+        else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
     } else {
-        if (cw == 8) edge_reg_packed_kernel<0, 4, 8, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
-        else edge_reg_packed_kernel<0, 4, 4, OUT, HALO><<<grid, kThreads, 0, st>>>(rp);
+        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp);
+        else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
     }
     return cuda_check("edge_reg_packed_kernel");
 }
@@ -178,11 +202,11 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, unsigned grid, cudaStream
 template <int OUT, bool HALO>
 int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
     if (rp.v8) {
-        if (rs == 8) edge_reg_u8_kernel<8, OUT, HALO, true><<<grid, kThreads, 0, st>>>(rp);
-        else edge_reg_u8_kernel<4, OUT, HALO, true><<<grid, kThreads, 0, st>>>(rp);
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, 0, st, rp);
     } else {
-        if (rs == 8) edge_reg_u8_kernel<8, OUT, HALO, false><<<grid, kThreads, 0, st>>>(rp);
-        else edge_reg_u8_kernel<4, OUT, HALO, false><<<grid, kThreads, 0, st>>>(rp);
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, 0, st, rp);
     }
     return cuda_check("edge_reg_u8_kernel");
 }
@@ -242,11 +266,11 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
 #define BE_WARPIMG(L)                                                                          \
     case L:                                                                                    \
         if (o_edges && o_eset)                                                                 \
-            edge_warp_img_kernel<L, kOutAny><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+            launch_k(edge_warp_img_kernel<L, kOutAny>, (unsigned)grid, 0, st, rp, groups, nimg); \
         else if (o_eset)                                                                       \
-            edge_warp_img_kernel<L, kOutEset><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+            launch_k(edge_warp_img_kernel<L, kOutEset>, (unsigned)grid, 0, st, rp, groups, nimg); \
         else                                                                                   \
-            edge_warp_img_kernel<L, kOutEdges><<<(unsigned)grid, kThreads, 0, st>>>(rp, groups, nimg); \
+            launch_k(edge_warp_img_kernel<L, kOutEdges>, (unsigned)grid, 0, st, rp, groups, nimg); \
         return cuda_check("edge_warp_img_kernel");
                 switch (lwpr) {
                     BE_WARPIMG(0)
@@ -272,14 +296,14 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const unsigned grid = (unsigned)g;
             const bool halo = above || below;
             if (rp.o_edges && rp.o_eset) {
-                if (halo) edge_roll_u8_kernel<kRSL, kOutAny, true><<<grid, kThreads, 0, st>>>(rp);
-                else edge_roll_u8_kernel<kRSL, kOutAny, false><<<grid, kThreads, 0, st>>>(rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutAny, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kOutAny, false>, grid, 0, st, rp);
             } else if (rp.o_eset) {
-                if (halo) edge_roll_u8_kernel<kRSL, kOutEset, true><<<grid, kThreads, 0, st>>>(rp);
-                else edge_roll_u8_kernel<kRSL, kOutEset, false><<<grid, kThreads, 0, st>>>(rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutEset, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kOutEset, false>, grid, 0, st, rp);
             } else {
-                if (halo) edge_roll_u8_kernel<kRSL, kOutEdges, true><<<grid, kThreads, 0, st>>>(rp);
-                else edge_roll_u8_kernel<kRSL, kOutEdges, false><<<grid, kThreads, 0, st>>>(rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutEdges, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kOutEdges, false>, grid, 0, st, rp);
             }
             return cuda_check("edge_roll_u8_kernel");
         }

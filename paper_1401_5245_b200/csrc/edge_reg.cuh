@@ -94,6 +94,8 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
 template <int SWAP, int RS, int CW, int OUT, bool HALO>
 __global__ void __launch_bounds__(kThreads)
 edge_reg_packed_kernel(const RegParams p) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
@@ -214,6 +216,8 @@ __device__ __forceinline__ void ldg_stream_v8(const void *p, uint4 &a, uint4 &b)
 template <int LWPR, int OUT>
 __global__ void __launch_bounds__(kThreads)
 edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int WPR = 1 << LWPR;
     constexpr int RPI = 32 >> LWPR;
     const int64_t img = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -261,6 +265,8 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
 template <int RS, int OUT, bool HALO, bool V8>
 __global__ void __launch_bounds__(kThreads)
 edge_reg_u8_kernel(const RegParams p) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
@@ -353,6 +359,8 @@ edge_reg_u8_kernel(const RegParams p) {
 template <int RSL, int OUT, bool HALO>
 __global__ void __launch_bounds__(kThreads)
 edge_roll_u8_kernel(const RegParams p) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int Q = 4;
     static_assert(RSL % Q == 0, "strip must be a multiple of the ring");
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;

@@ -143,9 +143,11 @@ __device__ __forceinline__ void issue_tile(const StreamParams &p, int64_t t, cha
                         p.in + g * p.in_row_bytes + b_lo, seg, bar);
     }
     if (has_above) tma_load_1d(stage + dst_off + b_lo, p.above + b_lo, seg, bar);
-    if (has_below)
-        tma_load_1d(stage + (int64_t)(p.R + 1) * p.raw_pitch + dst_off + b_lo, p.below + b_lo, seg,
-                    bar);
+    if (has_below) {
+        // global row nrows lands at staged row nrows - (g0 - 1) (R+1 for a full tile)
+        const int64_t bi = p.nrows - (g0 - 1);
+        tma_load_1d(stage + bi * p.raw_pitch + dst_off + b_lo, p.below + b_lo, seg, bar);
+    }
 }
 
 // ---- consumer ----------------------------------------------------------------

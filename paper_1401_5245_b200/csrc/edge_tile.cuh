@@ -79,6 +79,14 @@ __device__ __forceinline__ uint4 ldg_stream_v4(const void *p) {
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p); }
 
+// Programmatic dependent launch (no-ops unless launched with the PDL attribute):
+// wait until the previous grid on the stream has completed and its writes are
+// visible, and let the next grid start launching once this CTA's work is issued.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Nonzero-byte flags: bit 7 of each byte set iff the byte is nonzero.
 __device__ __forceinline__ uint32_t nz_bytes(uint32_t v) {
     return (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
@@ -178,6 +186,13 @@ edge_tile_kernel(const TileParams p) {
         const int nvalid = (int)min((int64_t)R, p.nrows - g0);
         const int64_t rs = p.in_stride * (U8 ? 1 : 4);             // bytes per row
         const char *base = (const char *)p.in + g0 * rs;
+        // staged main row r: inside the raster, or -- for a partial last tile of a
+        // slab -- the halo row below the slab (global row nrows), or nothing
+        auto row_at = [&](int r) -> const char * {
+            if (r < nvalid) return base + r * rs;
+            if (r == nvalid && nvalid < R) return (const char *)p.below;
+            return nullptr;
+        };
         constexpr int U = 4;
         for (int r0 = tid >> log_items; r0 < R; r0 += U * rstep) {
             if (KIND == kP32Vec || KIND == kP64Vec || KIND == kU8Vec) {
@@ -189,8 +204,8 @@ edge_tile_kernel(const TileParams p) {
                     const int r = r0 + u * rstep;
                     full[u] = false;
                     v[u] = make_uint4(0u, 0u, 0u, 0u);
-                    if (r < nvalid) {
-                        const char *row = base + r * rs;
+                    const char *row = r < R ? row_at(r) : nullptr;
+                    if (row != nullptr) {
                         if (U8) {
                             if (x0 + 16 <= p.w) { v[u] = ldg_stream_v4(row + x0); full[u] = true; }
                         } else if (pw0 < p.wp) {
@@ -206,8 +221,8 @@ edge_tile_kernel(const TileParams p) {
                         if (U8) {
                             uint32_t half = 0xFFFFu;
                             if (full[u]) half = pack16(v[u]);
-                            else if (r < nvalid && x0 < p.w)
-                                half = pack16_bytes((const uint8_t *)(base + r * rs), x0, p.w);
+                            else if (row_at(r) != nullptr && x0 < p.w)
+                                half = pack16_bytes((const uint8_t *)row_at(r), x0, p.w);
                             reinterpret_cast<uint16_t *>(srow)[2 * (c >> 1) + ((c & 1) ? 0 : 1)] =
                                 (uint16_t)half;
                         } else {
@@ -222,8 +237,7 @@ edge_tile_kernel(const TileParams p) {
                 for (int u = 0; u < U; ++u) {
                     const int r = r0 + u * rstep;
                     if (r < R)
-                        stage_item<KIND>(smem + (r + 1) * P + 4, r < nvalid ? base + r * rs : nullptr,
-                                         c, pw0, x0, p);
+                        stage_item<KIND>(smem + (r + 1) * P + 4, row_at(r), c, pw0, x0, p);
                 }
             }
         }

@@ -57,9 +57,22 @@ def run(cfg, iters=200):
         return {"cfg": cfg, "profiled_launches": int(os.environ.get("KB_NOGRAPH"))}
     g = torch.cuda.CUDAGraph()
     k = pool * max(1, iters // pool)
+    nstreams = int(os.environ.get("KB_STREAMS", "1"))
     with torch.cuda.graph(g):
-        for i in range(k):
-            step(i)
+        if nstreams == 1:
+            for i in range(k):
+                step(i)
+        else:
+            # independent batches on parallel graph branches (fork / join)
+            cur = torch.cuda.current_stream()
+            side = [torch.cuda.Stream() for _ in range(nstreams)]
+            for s_ in side:
+                s_.wait_stream(cur)
+            for i in range(k):
+                with torch.cuda.stream(side[i % nstreams]):
+                    step(i)
+            for s_ in side:
+                cur.wait_stream(s_)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
