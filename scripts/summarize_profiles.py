@@ -1,0 +1,139 @@
+"""Turn a gpurun_out/prof capture (scripts/gpu_profiles.sh) into the committed
+profiles/ summaries: launch list, per-config ncu metrics and traffic.json.
+
+    python scripts/summarize_profiles.py [round_tag]      (default r1)
+"""
+
+import csv
+import collections
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "gpurun_out", "prof")
+DST = os.path.join(ROOT, "profiles")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
+ALG = {"c1": 256 * 256 * 1.125, "c2": 4096 * 64 * 64 * 1.125, "c3": 8192 * 8192 * 0.25,
+       "c4": 65536 * 65536 * 0.25, "c5": 1024 * 2048 * 2048 * 1.125}
+WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput",
+        "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread", "Theoretical Occupancy",
+        "Achieved Occupancy", "Grid Size", "Block Size", "Executed Instructions", "SM Frequency",
+        "DRAM Frequency", "No Eligible", "Warp Cycles Per Issued Instruction"]
+
+
+def ncu_csv(rep, page, extra=()):
+    out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv", *extra], capture_output=True,
+                         text=True).stdout
+    return list(csv.reader(out.splitlines()))
+
+
+def launch_list():
+    path = os.path.join(SRC, "launches_bench_c2.csv")
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            k = (d["ID"], d["Kernel Name"])
+            per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    out = os.path.join(DST, f"{TAG}_launches_bench_c2.csv")
+    share = collections.Counter()
+    with open(out, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["id", "kernel", "duration_ns", "dram_read_bytes", "dram_write_bytes"])
+        for (i, name), m in per.items():
+            w.writerow([i, name, int(m.get("gpu__time_duration.sum", 0)),
+                        int(m.get("dram__bytes_read.sum", 0)), int(m.get("dram__bytes_write.sum", 0))])
+            share[name.split("(")[0]] += m.get("gpu__time_duration.sum", 0)
+    tot = sum(share.values())
+    return [(k, v / tot) for k, v in share.most_common()], len(per)
+
+
+def full(cfg):
+    rep = os.path.join(SRC, f"full_{cfg}.ncu-rep")
+    if not os.path.exists(rep):
+        return None
+    rows = ncu_csv(rep, "details")
+    h = rows[0]
+    m = {"kernel": None}
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        m["kernel"] = d.get("Kernel Name")
+        if d.get("Metric Name") in WANT:
+            m[d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
+    raw = ncu_csv(rep, "raw")
+    hdr, units, vals = raw[0], raw[1], raw[2]
+    rv = dict(zip(hdr, vals))
+    ru = dict(zip(hdr, units))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3,
+             "ms": 1e6}
+
+    def num(k):
+        try:
+            return float(rv[k].replace(",", "")) * scale.get(ru.get(k, ""), 1)
+        except (KeyError, ValueError):
+            return None
+
+    rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+    dur = num("gpu__time_duration.sum")
+    m["dram_bytes_read"] = rd
+    m["dram_bytes_write"] = wr
+    m["duration_ns"] = dur
+    stalls = {}
+    for k in hdr:
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+            v = num(k)
+            if v:
+                stalls[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = v
+    m["top_stalls"] = sorted(stalls.items(), key=lambda kv: -kv[1])[:5]
+    if dur:
+        m["alg_GBps_cold"] = ALG[cfg] / dur
+        m["dram_GBps"] = ((rd or 0) + (wr or 0)) / dur
+    return m
+
+
+def main():
+    os.makedirs(DST, exist_ok=True)
+    shares, nl = launch_list()
+    res = {c: full(c) for c in ("c1", "c2", "c3", "c4", "c5")}
+    traffic = {c: (m["dram_bytes_read"] or 0) + (m["dram_bytes_write"] or 0)
+               for c, m in res.items() if m}
+    with open(os.path.join(DST, "traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    lines = [f"# ncu summary ({TAG})", "",
+             "Captured by `scripts/gpu_profiles.sh` on one B200 (`ncu --set full --clock-control none`,",
+             "default cache control = flushed between replays, so durations are cold-cache and",
+             "serialised); summarised by `scripts/summarize_profiles.py`.  Bench numbers are NOT",
+             "taken under ncu.", "",
+             f"## Launch list of `python bench.py --config c2 --steps 200 --warmup 5 --no-cpu` ({nl} launches)",
+             "", "| kernel | share of GPU time |", "|---|---|"]
+    lines += [f"| `{k}` | {v:.1%} |" for k, v in shares]
+    lines += ["", "## Top kernel per config (one launch, full section set)", ""]
+    for c, m in res.items():
+        if not m:
+            continue
+        lines.append(f"### {c}: `{m['kernel']}`")
+        for k in WANT:
+            if k in m:
+                lines.append(f"- {k}: {m[k]}")
+        lines.append(f"- DRAM bytes read / written: {m['dram_bytes_read']:.0f} / {m['dram_bytes_write']:.0f} "
+                     f"(algorithmic {ALG[c]:.0f})")
+        if m.get("alg_GBps_cold"):
+            lines.append(f"- algorithmic GB/s at the cold ncu duration: {m['alg_GBps_cold']:.0f}; "
+                         f"DRAM GB/s: {m['dram_GBps']:.0f}")
+        lines.append(f"- top stall reasons (pc samples): {m['top_stalls']}")
+        lines.append("")
+    with open(os.path.join(DST, f"{TAG}_ncu_summary.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
