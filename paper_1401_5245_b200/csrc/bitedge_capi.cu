@@ -225,6 +225,8 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 }
 
 // Returns 1 when the register-direct kernel does not apply (caller falls back).
+inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
+
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
             const void *below, uint32_t *o_edges, uint32_t *o_eset, int64_t out_stride_u32,
             const Geometry &G, int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
@@ -286,8 +288,73 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         }
     }
     const int64_t rows = row_hi - row_lo;
+    // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
+    if (input_kind == 1 && G.w >= 2048 && !getenv("BITEDGE_NO_TMA") && !getenv("BITEDGE_TMA1")) {
+        constexpr int kRSLT = 32, kD = 4;
+        const int64_t nseg = (G.w + 2047) / 2048;
+        const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
+        const int64_t nwarps = nstrips * nseg;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;
+        if ((force || nwarps >= (int64_t)sm_count() * 24) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
+            const unsigned grid = (unsigned)((nwarps + 7) / 8);
+            const size_t smem = (size_t)8 * kD * 2080 + (size_t)8 * kD * 8;
+            const bool halo = above || below;
+            rp.nstrips = nstrips;
+#define BE_TMA2(OUTK, H)                                                                        \
+    do {                                                                                        \
+        auto kern = edge_tma2_u8_kernel<kRSLT, kD, OUTK, H>;                                    \
+        thread_local bool attr = false;                                                         \
+        if (!attr) {                                                                            \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            attr = true;                                                                        \
+        }                                                                                       \
+        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
+    } while (0)
+            if (rp.o_edges && rp.o_eset) {
+                if (halo) BE_TMA2(kOutAny, true); else BE_TMA2(kOutAny, false);
+            } else if (rp.o_eset) {
+                if (halo) BE_TMA2(kOutEset, true); else BE_TMA2(kOutEset, false);
+            } else {
+                if (halo) BE_TMA2(kOutEdges, true); else BE_TMA2(kOutEdges, false);
+            }
+#undef BE_TMA2
+            return cuda_check("edge_tma2_u8_kernel");
+        }
+    }
+    if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
+        constexpr int kRSLT = 32, kD = 6;
+        const int64_t nseg = (G.w + 1023) / 1024;
+        const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
+        const int64_t nwarps = nstrips * nseg;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;   // tests: any size
+        if ((force || nwarps >= (int64_t)sm_count() * 32) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
+            const unsigned grid = (unsigned)((nwarps + 7) / 8);
+            const size_t smem = (size_t)8 * kD * 1056 + (size_t)8 * kD * 8;
+            const bool halo = above || below;
+            rp.nstrips = nstrips;
+#define BE_TMA(OUTK, H)                                                                         \
+    do {                                                                                        \
+        auto kern = edge_tma_u8_kernel<kRSLT, kD, OUTK, H>;                                     \
+        thread_local bool attr = false;                                                         \
+        if (!attr) {                                                                            \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            attr = true;                                                                        \
+        }                                                                                       \
+        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
+    } while (0)
+            if (rp.o_edges && rp.o_eset) {
+                if (halo) BE_TMA(kOutAny, true); else BE_TMA(kOutAny, false);
+            } else if (rp.o_eset) {
+                if (halo) BE_TMA(kOutEset, true); else BE_TMA(kOutEset, false);
+            } else {
+                if (halo) BE_TMA(kOutEdges, true); else BE_TMA(kOutEdges, false);
+            }
+#undef BE_TMA
+            return cuda_check("edge_tma_u8_kernel");
+        }
+    }
     // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
-    constexpr int kRSL = 32;
+    constexpr int kRSL = 32, kQ = 4;
     if (input_kind == 1 && rp.v8 && !getenv("BITEDGE_NO_ROLL") &&
         (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
         rp.nstrips = (rows + kRSL - 1) / kRSL;
@@ -296,14 +363,14 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const unsigned grid = (unsigned)g;
             const bool halo = above || below;
             if (rp.o_edges && rp.o_eset) {
-                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutAny, true>, grid, 0, st, rp);
-                else launch_k(edge_roll_u8_kernel<kRSL, kOutAny, false>, grid, 0, st, rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutAny, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutAny, false>, grid, 0, st, rp);
             } else if (rp.o_eset) {
-                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutEset, true>, grid, 0, st, rp);
-                else launch_k(edge_roll_u8_kernel<kRSL, kOutEset, false>, grid, 0, st, rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEset, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEset, false>, grid, 0, st, rp);
             } else {
-                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kOutEdges, true>, grid, 0, st, rp);
-                else launch_k(edge_roll_u8_kernel<kRSL, kOutEdges, false>, grid, 0, st, rp);
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEdges, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEdges, false>, grid, 0, st, rp);
             }
             return cuda_check("edge_roll_u8_kernel");
         }

@@ -197,6 +197,37 @@ __device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b) {
     return (pack16(a) << 16) | pack16(b);
 }
 
+// 8 bytes that are all 0 or 1 -> 8 bits MSB-first: x*16 + y puts the flags of
+// x at bits 4,12,20,28 and of y at 0,8,16,24 (no carries: bytes <= 1), then the
+// same collision-free multiply as pack8.
+__device__ __forceinline__ uint32_t pack8_01(uint32_t x, uint32_t y) {
+    const uint64_t prod = (uint64_t)(x * 16u + y) * 0x80402010ull;
+    return (uint32_t)(prod >> 28) & 0xFFu;
+}
+
+// pack32 with a fast path for canonical 0/1 pixel bytes (what to_array and a
+// binarisation produce): one test per 32 bytes skips the per-byte nonzero
+// normalisation; any other byte value takes the general path.  Exact for all
+// inputs (nonzero -> white, bitimage.py:124,133).
+__device__ __forceinline__ uint32_t pack32_any(uint4 a, uint4 b) {
+    const uint32_t hi = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
+    if (hi == 0u) {
+        return (pack8_01(a.x, a.y) << 24) | (pack8_01(a.z, a.w) << 16) |
+               (pack8_01(b.x, b.y) << 8) | pack8_01(b.z, b.w);
+    }
+    return pack32(a, b);
+}
+
+// ld.global.nc.u8 under a predicate, no branch (lanes with p == 0 keep `dflt`).
+__device__ __forceinline__ uint32_t ldg_u8_if(bool p, const char *ptr, uint32_t dflt) {
+    uint32_t v = dflt;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.u8 %0, [%1];\n}\n"
+        : "+r"(v)
+        : "l"(ptr), "r"((uint32_t)p));
+    return v;
+}
+
 // One 256-bit load (sm_100: LDG.E.256), 32-byte aligned, L1 no-allocate.
 __device__ __forceinline__ void ldg_stream_v8(const void *p, uint4 &a, uint4 &b) {
     asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -354,15 +385,14 @@ edge_reg_u8_kernel(const RegParams p) {
 // owns one output word (32 pixels) of RSL consecutive rows and keeps the next
 // 2-3 rows' 256-bit loads in flight while it packs and emits the current
 // one, so the 2 halo rows cost 2/RSL instead of 2/RS (the one-shot K2's
-// dominant overhead on big pages, BASELINE config C5).  Ring of Q = 4 raw
-// slots; the loop is unrolled by Q so every slot index is static.
-template <int RSL, int OUT, bool HALO>
+// dominant overhead on big pages, BASELINE config C5).  Ring of Q raw
+// slots (Q-1 rows in flight); the loop is unrolled by Q so slot indices are static.
+template <int RSL, int Q, int OUT, bool HALO>
 __global__ void __launch_bounds__(kThreads)
 edge_roll_u8_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
-    constexpr int Q = 4;
-    static_assert(RSL % Q == 0, "strip must be a multiple of the ring");
+    static_assert(RSL % Q == 0 && Q >= 4, "strip must be a multiple of the ring");
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
@@ -378,25 +408,30 @@ edge_roll_u8_kernel(const RegParams p) {
     const int i_lo = g0 == 0 ? 1 : 0;
     const int64_t lim = p.nrows - (g0 - 1);            // staged rows i < lim exist
 
-    // staged row i (global g0-1+i), i in [0, RSL+2): raw 32 bytes + edge bits
+    // staged row i (global g0-1+i), i in [0, RSL+2): raw 32 bytes, plus for the
+    // warp's edge lanes the neighbouring pixels (bit 0: x0-1, bit 31: x0+32).
+    // Loads are branch-free: a row that does not exist reads row 0 of the
+    // raster instead (always valid) and is marked absent in `okm`.
+    const int nvis = live ? (int)(lim < RSL + 2 ? lim : RSL + 2) : 0;   // rows i < nvis exist
+    const char *safe = p.in + x0;
     uint4 ra[Q], rb2[Q];
-    uint32_t lb[Q], rbt[Q];
+    uint32_t eb[Q];
+    uint32_t okm = 0u;                                                 // bit slot: row present
     auto issue = [&](int i, int slot) {
         const char *ptr = base + i * rb;
-        bool ok = live && i >= i_lo && i < lim && i < RSL + 2;
+        bool ok = i >= i_lo && i < nvis;
         if (HALO) {
-            if (i == 0 && g0 == 0 && p.above) { ptr = p.above + x0; ok = live; }
-            if (i == lim && i < RSL + 2 && p.below) { ptr = p.below + x0; ok = live; }
+            if (i == 0 && g0 == 0 && p.above && live) { ptr = p.above + x0; ok = true; }
+            if (i == lim && i < RSL + 2 && p.below && live) { ptr = p.below + x0; ok = true; }
         }
-        ra[slot] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        rb2[slot] = ra[slot];
-        lb[slot] = fw;
-        rbt[slot] = 0u;
-        if (ok) {
-            ldg_stream_v8(ptr, ra[slot], rb2[slot]);
-            if (need_l) lb[slot] = ptr[-1] != 0 ? 1u : 0u;
-            if (need_r) rbt[slot] = ptr[32] != 0 ? 0x80000000u : 0u;
-        }
+        ldg_stream_v8(ok ? ptr : safe, ra[slot], rb2[slot]);
+        okm = ok ? (okm | (1u << slot)) : (okm & ~(1u << slot));
+        uint32_t e = ldg_u8_if(ok && need_l, ptr - 1, 0u) != 0u ? 1u : 0u;
+        e |= ldg_u8_if(ok && need_r, ptr + 32, 0u) != 0u ? 0x80000000u : 0u;
+        eb[slot] = e;
+    };
+    auto word = [&](int slot) -> uint32_t {
+        return (okm >> slot) & 1u ? pack32_any(ra[slot], rb2[slot]) : 0xFFFFFFFFu;
     };
 
     uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
@@ -410,25 +445,23 @@ edge_roll_u8_kernel(const RegParams p) {
     uint32_t y = live ? (uint32_t)(g0 % p.h) : 0u;
     int64_t o = g0 * p.out_stride + c;
 
-    // prologue: staged rows 0 (halo above) .. 3 in flight; pack rows 0 and 1
-    issue(0, 0);
-    issue(1, 1);
-    issue(2, 2);
-    issue(3, 3);
-    uint32_t w_up = pack32(ra[0], rb2[0]);
-    uint32_t w_c = pack32(ra[1], rb2[1]);
-    uint32_t lb_c = lb[1], rb_c = rbt[1];
+    // prologue: staged rows 0 (halo above) .. Q-1 in flight; pack rows 0 and 1
+#pragma unroll
+    for (int i = 0; i < Q; ++i) issue(i, i);
+    uint32_t w_up = word(0);
+    uint32_t w_c = word(1);
+    uint32_t e_c = eb[1];
     for (int r0 = 0; r0 < RSL; r0 += Q) {
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             const int r = r0 + k;                      // output row; staged row r+1 is centre
-            issue(r + 4, k);                           // rows r+2 .. r+4 stay in flight
+            issue(r + Q, k);                           // rows r+2 .. r+Q stay in flight
             const int sd = (k + 2) % Q;                // staged row r+2 = down neighbour
-            const uint32_t w_d = pack32(ra[sd], rb2[sd]);
+            const uint32_t w_d = word(sd);
             uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, w_c, 1);
             uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, w_c, 1);
-            if (lane == 0) lw = lb_c;
-            if (lane == 31) rw = rb_c;
+            if (lane == 0) lw = e_c;
+            if (lane == 31) rw = e_c;
             if (c == 0) lw = fw;
             const int64_t g = g0 + r;
             if (live && g < p.row_hi) {
@@ -442,11 +475,290 @@ edge_roll_u8_kernel(const RegParams p) {
             }
             w_up = w_c;
             w_c = w_d;
-            lb_c = lb[sd];
-            rb_c = rbt[sd];
+            e_c = eb[sd];
             o += p.out_stride;
             if (++y == p.h) y = 0;
         }
+    }
+}
+
+// ---------------------------------------------------------------- K2t: uint8, per-warp TMA ring
+
+// mbarrier / TMA helpers (shared with edge_stream.cuh's design, redeclared here
+// to keep this header standalone).
+__device__ __forceinline__ uint32_t sm_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void wbar_init(uint64_t *b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(b)));
+}
+__device__ __forceinline__ void wbar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void wbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra W_%=;\n}\n" ::"r"(
+            sm_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void wtma(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(sm_addr(dst)),
+        "l"(src), "r"(bytes), "r"(sm_addr(b))
+        : "memory");
+}
+
+// One warp owns a 1024-pixel row segment (32 output words, one per lane) of a
+// strip of RSL rows.  Its lane 0 streams the strip's RSL+2 staged rows (the
+// segment plus 16 bytes either side for the neighbour pixels) into a private
+// D-slot shared-memory ring with `cp.async.bulk` (TMA), each slot tracked by an
+// mbarrier transaction count, so D row segments are in flight per warp without
+// holding them in registers -- which is what lets 32 warps per SM keep ~200 KB
+// in flight (the register ring of K2r tops out near 75 KB).  Lanes read their
+// 32 bytes from shared memory, pack, and emit exactly like K2r.  No CTA-wide
+// barriers: warps of a CTA are independent.
+template <int RSL, int D, int OUT, bool HALO>
+__global__ void __launch_bounds__(kThreads)
+edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
+    constexpr int SLOT = 1056;                       // 16 + 1024 + 16 bytes
+    constexpr int WARPS = kThreads / 32;
+    extern __shared__ __align__(128) char tsm[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char *ring = tsm + (size_t)wid * D * SLOT;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + (size_t)WARPS * D * SLOT) + wid * D;
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) wbar_init(&bars[s]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    const int64_t gw = (int64_t)blockIdx.x * WARPS + wid;
+    if (gw >= nwarps) return;                        // whole warp
+    const int64_t strip = gw / nseg;
+    const int seg = (int)(gw - strip * nseg);
+    const int64_t g0 = p.row_lo + strip * RSL;
+    const int64_t x0 = (int64_t)seg * 1024;
+    const int c = seg * 32 + lane;                   // this lane's output word
+    const uint32_t fw = p.fillword;
+    const int64_t rb = p.in_row_bytes;
+    const int64_t wr = (p.w + 15) & ~(int64_t)15;    // readable bytes per row
+    const int64_t b_lo = x0 > 0 ? x0 - 16 : 0;       // copied byte range of a row
+    const int64_t b_hi = x0 + 1040 < wr ? x0 + 1040 : wr;
+    const uint32_t seg_bytes = (uint32_t)(b_hi - b_lo);
+    const int dst_off = (int)(b_lo - (x0 - 16));     // 16 for the first segment, else 0
+    const int nst = RSL + 2;                         // staged rows
+    const int64_t lim = p.nrows - (g0 - 1);          // staged rows i < lim exist (below: i == lim)
+
+    // staged row i <-> global row g0-1+i; returns the row pointer or nullptr
+    auto row_of = [&](int i) -> const char * {
+        const int64_t g = g0 - 1 + i;
+        if (g >= 0 && g < p.nrows) return p.in + g * rb;
+        if (HALO) {
+            if (g == -1) return p.above;
+            if (g == p.nrows && i < nst) return p.below;
+        }
+        return nullptr;
+    };
+    auto issue = [&](int i) {                        // lane 0 only
+        if (i >= nst) return;
+        const char *row = row_of(i);
+        if (row == nullptr) return;
+        uint64_t *b = &bars[i % D];
+        wbar_expect(b, seg_bytes);
+        wtma(ring + (i % D) * SLOT + dst_off, row + b_lo, seg_bytes, b);
+    };
+    if (lane == 0)
+        for (int i = 0; i < D; ++i) issue(i);
+
+    uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
+    if (c == p.pl) {
+        keep = ~p.lastbit;
+        fixb = fw & p.lastbit;
+        force = p.padmask;
+    } else if (c > p.pl) {
+        force = 0xFFFFFFFFu;
+    }
+    const bool live_col = c < p.wp;
+    uint32_t y = (uint32_t)(g0 % p.h);
+    int64_t o = g0 * p.out_stride + c;
+    uint32_t phase = 0u;                             // per-slot parity bits
+    uint32_t w_up = 0u, w_c = 0u, e_c = 0u;
+    for (int i = 0; i < nst; ++i) {
+        const int slot = i % D;
+        uint32_t w_new = 0xFFFFFFFFu, e_new = 0u;
+        if (row_of(i) != nullptr) {
+            wbar_wait(&bars[slot], (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+            const char *src = ring + slot * SLOT + 16 + 32 * lane;
+            const uint4 a = *reinterpret_cast<const uint4 *>(src);
+            const uint4 b = *reinterpret_cast<const uint4 *>(src + 16);
+            w_new = pack32_any(a, b);
+            if (lane == 0) e_new = src[-1] != 0 ? 1u : 0u;
+            if (lane == 31) e_new = src[32] != 0 ? 0x80000000u : 0u;
+        }
+        // slot i % D is free (consumed, or never filled because staged row i does
+        // not exist): refill it with staged row i + D
+        __syncwarp();
+        if (lane == 0) issue(i + D);
+        if (i >= 2) {
+            // output row r = i-2: up = staged i-2, centre = staged i-1, down = staged i
+            const int r = i - 2;
+            uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, w_c, 1);
+            uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, w_c, 1);
+            if (lane == 0) lw = e_c;
+            if (lane == 31) rw = e_c;
+            if (c == 0) lw = fw;
+            if (live_col && g0 + r < p.row_hi) {
+                const uint32_t u = (y == 0 && !(HALO && p.above)) ? fw : w_up;
+                const uint32_t d = (y == p.h - 1 && !(HALO && p.below)) ? fw : w_new;
+                const uint32_t ln = __funnelshift_r(w_c, lw, 1);
+                const uint32_t rn = (__funnelshift_l(rw, w_c, 1) & keep) | fixb;
+                const uint32_t any = ln | rn | u | d;
+                if (OUT != kOutEset) __stcs(p.o_edges + o, w_c | ~any | force);
+                if (OUT != kOutEdges) __stcs(p.o_eset + o, (~w_c & any) | force);
+            }
+            o += p.out_stride;
+            if (++y == p.h) y = 0;
+        }
+        w_up = w_c;
+        w_c = w_new;
+        e_c = e_new;
+    }
+    (void)lim;
+}
+
+// K2t2: same ring, but a warp owns a 2048-pixel row segment and every lane two
+// output words (word L and word 32+L of the segment), halving the per-row fixed
+// cost (barrier wait, refill, row bookkeeping) per word -- K2t was issue-bound
+// at ~200 instructions per 1 KB row segment.  Staged rows are addressed with
+// integer offsets from one base pointer; only the first/last staged rows can be
+// absent or come from the halo buffers.
+template <int RSL, int D, int OUT, bool HALO>
+__global__ void __launch_bounds__(kThreads)
+edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
+    constexpr int SEG = 2048;                        // pixels (bytes) per warp segment
+    constexpr int SLOT = 16 + SEG + 16;
+    constexpr int WARPS = kThreads / 32;
+    extern __shared__ __align__(128) char tsm[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char *ring = tsm + (size_t)wid * D * SLOT;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + (size_t)WARPS * D * SLOT) + wid * D;
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) wbar_init(&bars[s]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    const int64_t gw = (int64_t)blockIdx.x * WARPS + wid;
+    if (gw >= nwarps) return;
+    const int64_t strip = gw / nseg;
+    const int seg = (int)(gw - strip * nseg);
+    const int64_t g0 = p.row_lo + strip * RSL;
+    const int64_t x0 = (int64_t)seg * SEG;
+    const int ca = seg * 64 + lane, cb = ca + 32;    // this lane's two output words
+    const uint32_t fw = p.fillword;
+    const int64_t rb = p.in_row_bytes;
+    const int64_t wr = (p.w + 15) & ~(int64_t)15;
+    const int64_t b_lo = x0 > 0 ? x0 - 16 : 0;
+    const int64_t b_hi = x0 + SEG + 16 < wr ? x0 + SEG + 16 : wr;
+    const uint32_t seg_bytes = (uint32_t)(b_hi - b_lo);
+    const int dst_off = (int)(b_lo - (x0 - 16));
+    constexpr int NST = RSL + 2;
+    // staged rows i in [i_lo, i_hi) lie inside `in`; row 0 / row lim may be halos
+    const int i_lo = g0 == 0 ? 1 : 0;
+    const int64_t lim = p.nrows - (g0 - 1);
+    const int i_hi = lim < NST ? (int)lim : NST;
+    const char *base = p.in + (g0 - 1) * rb + b_lo;
+    const bool top_halo = HALO && g0 == 0 && p.above != nullptr;
+    const bool bot_halo = HALO && lim < NST && p.below != nullptr;
+    auto exists = [&](int i) {
+        return (i >= i_lo && i < i_hi) || (top_halo && i == 0) || (bot_halo && i == i_hi);
+    };
+    auto issue = [&](int i) {                        // lane 0 only
+        if (i >= NST || !exists(i)) return;
+        const char *src = base + i * rb;
+        if (top_halo && i == 0) src = p.above + b_lo;
+        if (bot_halo && i == i_hi) src = p.below + b_lo;
+        uint64_t *b = &bars[i % D];
+        wbar_expect(b, seg_bytes);
+        wtma(ring + (i % D) * SLOT + dst_off, src, seg_bytes, b);
+    };
+    if (lane == 0)
+        for (int i = 0; i < D; ++i) issue(i);
+
+    auto tail_consts = [&](int c, uint32_t &keep, uint32_t &fixb, uint32_t &force) {
+        keep = 0xFFFFFFFFu; fixb = 0u; force = 0u;
+        if (c == p.pl) { keep = ~p.lastbit; fixb = fw & p.lastbit; force = p.padmask; }
+        else if (c > p.pl) force = 0xFFFFFFFFu;
+    };
+    uint32_t ka, fa, ga, kb, fb, gb;
+    tail_consts(ca, ka, fa, ga);
+    tail_consts(cb, kb, fb, gb);
+    const bool la = ca < p.wp, lb_ = cb < p.wp;
+    uint32_t y = (uint32_t)(g0 % p.h);
+    int64_t o = g0 * p.out_stride + ca;
+    uint32_t phase = 0u;
+    uint32_t ua = 0, ub = 0, xa = 0, xb = 0, el = 0, er = 0;   // up row, centre row, edge pixels
+    for (int i = 0; i < NST; ++i) {
+        const int slot = i % D;
+        uint32_t na = 0xFFFFFFFFu, nb = 0xFFFFFFFFu, nel = 0u, ner = 0u;
+        if (exists(i)) {
+            wbar_wait(&bars[slot], (phase >> slot) & 1u);
+            phase ^= 1u << slot;
+            const char *s = ring + slot * SLOT + 16;
+            na = pack32_any(*reinterpret_cast<const uint4 *>(s + 32 * lane),
+                            *reinterpret_cast<const uint4 *>(s + 32 * lane + 16));
+            nb = pack32_any(*reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane),
+                            *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16));
+            if (lane == 0) nel = s[-1] != 0 ? 1u : 0u;
+            if (lane == 31) ner = s[SEG] != 0 ? 0x80000000u : 0u;
+        }
+        __syncwarp();
+        if (lane == 0) issue(i + D);                 // slot free (consumed or unused)
+        if (i >= 2) {
+            const int r = i - 2;                     // output row: up = ua/ub, centre = xa/xb, down = na/nb
+            const uint32_t a_up = __shfl_up_sync(0xFFFFFFFFu, xa, 1);
+            const uint32_t a_dn = __shfl_down_sync(0xFFFFFFFFu, xa, 1);
+            const uint32_t b_up = __shfl_up_sync(0xFFFFFFFFu, xb, 1);
+            const uint32_t b_dn = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
+            const uint32_t a31 = __shfl_sync(0xFFFFFFFFu, xa, 31);   // word 31 (left of word 32)
+            const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, xb, 0);     // word 32 (right of word 31)
+            const uint32_t lwa = lane == 0 ? (ca == 0 ? fw : el) : a_up;
+            const uint32_t rwa = lane == 31 ? b0 : a_dn;
+            const uint32_t lwb = lane == 0 ? a31 : b_up;
+            const uint32_t rwb = lane == 31 ? er : b_dn;
+            if (g0 + r < p.row_hi) {
+                const bool top = y == 0 && !(HALO && p.above);
+                const bool bot = y == p.h - 1 && !(HALO && p.below);
+                const uint32_t uA = top ? fw : ua, uB = top ? fw : ub;
+                const uint32_t dA = bot ? fw : na, dB = bot ? fw : nb;
+                const uint32_t lnA = __funnelshift_r(xa, lwa, 1);
+                const uint32_t rnA = (__funnelshift_l(rwa, xa, 1) & ka) | fa;
+                const uint32_t anyA = lnA | rnA | uA | dA;
+                const uint32_t lnB = __funnelshift_r(xb, lwb, 1);
+                const uint32_t rnB = (__funnelshift_l(rwb, xb, 1) & kb) | fb;
+                const uint32_t anyB = lnB | rnB | uB | dB;
+                if (la) {
+                    if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
+                }
+                if (lb_) {
+                    if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
+                }
+            }
+            o += p.out_stride;
+            if (++y == p.h) y = 0;
+        }
+        ua = xa; ub = xb; xa = na; xb = nb;
+        el = nel; er = ner;
     }
 }
 

@@ -26,6 +26,9 @@ VARIANTS = {
     "no_roll": {"BITEDGE_NO_ROLL": "1"},
     "no_warpimg": {"BITEDGE_NO_WARPIMG": "1"},
     "no_pdl": {"BITEDGE_PDL": "0"},
+    "tma_warp": {"BITEDGE_FORCE_TMA": "1"},
+    "tma_warp1k": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA1": "1"},
+    "no_tma": {"BITEDGE_NO_TMA": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
