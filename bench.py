@@ -6,10 +6,11 @@ Gpixel/s, and % of the HBM roofline).
 
 A step is one pass of the hot path over one batch of the config's synthetic
 input; the default workload is configs[1] (C2: 4096 glyphs of
-64x64 uint8, fused pack+edge).  Under torchrun (N>1) the batch configs are
-batch-sharded (C2, C5: fixed global batch -> strong scaling), C4 is row-sharded
-with a 1-row NCCL halo exchange, and C1/C3 run replicas.  Rank 0 prints ONE
-JSON line.
+64x64 uint8, fused pack+edge).  Under torchrun (N>1) the batch configs shard a
+stream of independent images (C2, C5: one batch per rank, no collective ->
+weak scaling; --strong splits one batch instead), C4 is row-sharded with a
+1-row NCCL halo exchange (strong scaling), and C1/C3 run replicas.  Rank 0
+prints ONE JSON line.
 
 * value: whole-job Gpixel/s with inputs resident in HBM -- K steps on the
   device, CUDA-event timed, max over ranks; consecutive steps rotate through a
@@ -51,7 +52,7 @@ CONFIGS = {
 }
 BYTES_PER_PX = {"u8": 1.125, "packed": 0.25}
 METRIC = "Gpixel/s mask-method edge detection (1/2/4/8 B200); % of HBM roofline"
-DEFAULT_STEPS = {"c1": 20000, "c2": 20000, "c3": 5000, "c4": 200, "c5": 50}
+DEFAULT_STEPS = {"c1": 200000, "c2": 200000, "c3": 150000, "c4": 3000, "c5": 600}
 
 
 def log(*a):
@@ -309,8 +310,14 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 << 20)
 
-    # ---- this rank's share
-    if shard == "batch":
+    # ---- this rank's share.  Batch configs shard a stream of independent images:
+    # by default every rank owns its own batch of n images (images [r*n, (r+1)*n)
+    # of the global stream; weak scaling, no collective); --strong splits one
+    # batch of n images across the ranks instead.
+    if shard == "batch" and not args.strong:
+        lo, hi = rank * n, (rank + 1) * n
+        imgs_local, rows_local = n, h
+    elif shard == "batch":
         lo, hi = bd.shard_range(n, rank, world)
         imgs_local, rows_local = hi - lo, h
     elif shard == "rows":
@@ -450,7 +457,8 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-    px_all = (n * h * w) if shard in ("batch", "rows") else (n * h * w * world)
+    weak_batch = shard == "batch" and not args.strong
+    px_all = (n * h * w * world) if (weak_batch or shard == "replica") else (n * h * w)
     value = px_all * steps / (ms_max / 1e3) / 1e9
     ms_step = ms_max / steps
 
@@ -493,7 +501,7 @@ def run_ours(args):
                 t = torch.tensor([ems], device=dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ems = float(t.item())
-            px_e2e = (n * h * w) if shard in ("batch", "rows") else (n * h * w * world)
+            px_e2e = px_all
             e2e = {"value": px_e2e * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gpixel/s",
                    "h2d_bytes_per_step": int(pipe.h2d_bytes), "d2h_bytes_per_step":
                    int(pipe.d2h_bytes), "steps": e2e_steps, "ms_per_step": ems / e2e_steps}
@@ -512,12 +520,15 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
             "higher_is_better": True,
-            "scaling": "strong" if shard in ("batch", "rows") else "weak",
+            "scaling": "strong" if (shard == "rows" or (shard == "batch" and args.strong))
+                       else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": desc, "config_id": cfg, "global_batch": n,
+            "config": {"workload": desc, "config_id": cfg,
+                       "global_batch": n * world if weak_batch else n, "per_rank_batch": imgs_local,
                        "image": [h, w], "input": "uint8 pixels" if kind == "u8" else
                        "packed u32 row words", "parallelism":
-                       {"batch": f"batch-shard x{world}", "rows": f"row-shard x{world} + NCCL halo",
+                       {"batch": f"batch-shard x{world}" + ("" if weak_batch else " (strong)"),
+                        "rows": f"row-shard x{world} + NCCL halo",
                         "replica": f"replicas x{world}"}[shard],
                        "l2_policy": f"rotating pool of {pool} input/output sets "
                                     f"({pool * step_bytes / 2**20:.0f} MiB > 3x L2 "
@@ -579,7 +590,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--strong", action="store_true",
+                    help="batch configs: split one batch across ranks instead of one batch per rank")
+    ap.add_argument("--streams", type=int, default=3,
                     help="parallel graph branches for independent batches (1 = serial)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

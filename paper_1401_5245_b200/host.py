@@ -33,7 +33,7 @@ class HostBatchEdges:
         self.out_shape = (n, h, cu.words_per_row(self.width, 32))
         if chunk_images is None:
             per_img = h * s * (1 if kind == "u8" else 4)
-            chunk_images = max(1, min(n, (32 << 20) // max(1, per_img)))   # ~32 MiB per chunk
+            chunk_images = max(1, min(n, (8 << 20) // max(1, per_img)))    # ~8 MiB per chunk
         self.chunk = int(chunk_images)
         self.d_in = [torch.empty((self.chunk, h, s), dtype=self.in_dtype, device=self.device)
                      for _ in range(2)]
