@@ -76,10 +76,10 @@ class RowShardedEdges:
     `slab` is an int32 CUDA tensor [rows, S] of MSB-first row words; the
     result lands in `self.out` (same shape)."""
 
-    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None):
-        from . import cuda as _cuda
-
-        self._cuda = _cuda
+    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None, compute=None):
+        """`compute(slab, above, below, out, row_lo, row_hi)` computes output rows
+        [row_lo, row_hi) of the slab; the default is kernel K3 through the C ABI
+        (the CPU tests substitute the oracle to exercise this orchestration)."""
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.group = group
@@ -88,29 +88,33 @@ class RowShardedEdges:
         self.border = border
         self.rows = slab.shape[0]
         s = slab.shape[1]
-        # halo buffers padded to a 16-byte multiple so the kernel's 128-bit loads stay in bounds
-        pad = (s + 3) // 4 * 4
+        # halo buffers padded to a 32-byte multiple so 256-bit loads stay in bounds
+        pad = (s + 7) // 8 * 8
         self.above = torch.empty(pad, dtype=slab.dtype, device=slab.device)
         self.below = torch.empty(pad, dtype=slab.dtype, device=slab.device)
         self.out = torch.empty_like(slab)
+        if compute is None:
+            from . import cuda as _cuda
+
+            def compute(sl, ab, be, out, lo, hi):
+                _cuda.edges_halo(sl, ab, be, self.width, self.border, out=out, row_lo=lo,
+                                 row_hi=hi)
+        self.compute = compute
 
     def step(self) -> torch.Tensor:
-        cu, rows = self._cuda, self.rows
-        works = exchange_halos(self.slab[0], self.slab[rows - 1], self.above[: self.slab.shape[1]],
-                               self.below[: self.slab.shape[1]], self.rank, self.world, self.group)
+        rows, s = self.rows, self.slab.shape[1]
+        works = exchange_halos(self.slab[0], self.slab[rows - 1], self.above[:s], self.below[:s],
+                               self.rank, self.world, self.group)
         above = self.above if self.rank > 0 else None
         below = self.below if self.rank < self.world - 1 else None
         if not works:
-            cu.edges_halo(self.slab, None, None, self.width, self.border, out=self.out)
+            self.compute(self.slab, None, None, self.out, 0, rows)
             return self.out
         if rows > 2:  # interior rows need no halo: overlap them with the exchange
-            cu.edges_halo(self.slab, None, None, self.width, self.border, out=self.out,
-                          row_lo=1, row_hi=rows - 1)
+            self.compute(self.slab, None, None, self.out, 1, rows - 1)
         for w in works:
             w.wait()
-        cu.edges_halo(self.slab, above, below, self.width, self.border, out=self.out,
-                      row_lo=0, row_hi=1)
+        self.compute(self.slab, above, below, self.out, 0, 1)
         if rows > 1:
-            cu.edges_halo(self.slab, above, below, self.width, self.border, out=self.out,
-                          row_lo=rows - 1, row_hi=rows)
+            self.compute(self.slab, above, below, self.out, rows - 1, rows)
         return self.out

@@ -72,6 +72,52 @@ def _worker(rank, world, port, H, W, seed, q):
         dist.destroy_process_group()
 
 
+def _worker_rowshard(rank, world, port, H, W, seed, q):
+    """RowShardedEdges orchestration (exchange, interior rows while in flight, the two
+    boundary rows after) with the C oracle standing in for kernel K3."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import cscan
+        from oracle import port as P
+        from paper_1401_5245_b200.dist import RowShardedEdges
+
+        rng = np.random.default_rng(seed)
+        img = (rng.random((H, W)) < 0.5).astype(np.uint8)
+        packed = P.pack_u32(img)
+        lo, hi = shard_range(H, rank, world)
+        slab = torch.from_numpy(packed[lo:hi].view(np.int32).copy())
+        calls = []
+
+        def oracle_k3(sl, ab, be, out, r0, r1):
+            calls.append((r0, r1, ab is not None, be is not None))
+            a = None if ab is None else ab.numpy().view(np.uint32)[: sl.shape[1]]
+            b = None if be is None else be.numpy().view(np.uint32)[: sl.shape[1]]
+            full = cscan.scan_p32_slab(sl.numpy().view(np.uint32), a, b, W, 1)
+            out[r0:r1] = torch.from_numpy(full[r0:r1].view(np.int32))
+
+        rs = RowShardedEdges(slab, W, 1, compute=oracle_k3)
+        out = rs.step().numpy().view(np.uint32).copy()
+        obj = [None] * world
+        dist.all_gather_object(obj, (lo, out, calls))
+        if rank == 0:
+            full = np.concatenate([o[1] for o in sorted(obj, key=lambda t: t[0])])
+            ok = bool((full == cscan.scan_p32(packed, W, 1)).all())
+            # interior first, without halos; boundary rows after, with them
+            ok &= all(c[0][2:] == (False, False) for _, _, c in obj if len(c) > 1)
+            q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_edges_orchestration_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker_rowshard, args=(world, _free_port(), 47, 130, 11, q), nprocs=world, join=True)
+    assert q.get(timeout=60) is True
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_row_shard_halo_exchange_gloo(world):
     ctx = mp.get_context("spawn")
