@@ -492,8 +492,8 @@ def run_ours(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(e2e_steps):
-                pipe(hin, hout, sync=False)
-                _ = int(hout[0, 0, 0])      # the step's result read back on the host
+                pipe(hin, hout, sync=True)  # waits for this step's D2H
+                _ = int(hout[0, 0, 0])      # the step's result, read on the host
             e1.record()
             torch.cuda.synchronize()
             ems = e0.elapsed_time(e1)

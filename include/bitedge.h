@@ -135,6 +135,20 @@ int be_count_black(const void *in, int64_t *counts, int word_bits, int64_t n, in
 int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
                   int64_t row_stride_words, int fill_bit, void *stream);
 
+/* ---- host buffers (the end-to-end path) ----------------------------------- */
+
+/* Edges of a batch that lives in HOST memory (pinned for overlap): uint8 pixels
+ * [n][h][w] (input_kind 1, from_array + detect_edges_mask) or packed uint32 rows
+ * [n][h][ceil(w/32)] (input_kind 0) -> host_out uint32 [n][h][ceil(w/32)].  The
+ * batch is moved in chunks of chunk_images through two caller-provided device
+ * buffer pairs (dev_in[i] >= chunk * input image bytes, dev_out[i] >= chunk *
+ * output image bytes); chunk c runs H2D -> kernel -> D2H on stream (c % 2), so
+ * copies in both directions overlap the kernels.  blocking != 0 waits for both
+ * streams before returning. */
+int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
+                  int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
+                  int64_t chunk_images, void *stream0, void *stream1, int blocking);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);
 int be_abi_version(void);

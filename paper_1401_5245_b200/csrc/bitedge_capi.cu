@@ -887,4 +887,48 @@ int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h
     return cuda_check("scan_kernel");
 }
 
+int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
+                  int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
+                  int64_t chunk_images, void *stream0, void *stream1, int blocking) {
+    Geometry G;
+    int rc = make_geometry(G, 32, n, h, w, fill_bit);
+    if (rc) return rc;
+    if (n == 0) return BE_OK;
+    if (!host_in || !host_out || !dev_in || !dev_out || !dev_in[0] || !dev_in[1] || !dev_out[0] ||
+        !dev_out[1])
+        return fail(BE_EINVAL, "host / device buffers must not be NULL");
+    if (input_kind != 0 && input_kind != 1)
+        return fail(BE_EINVAL, "input_kind must be 0 (packed u32) or 1 (uint8)");
+    if (chunk_images < 1) return fail(BE_EINVAL, "chunk_images must be >= 1");
+    const int64_t wp = G.wp;
+    const size_t in_img = (size_t)h * (input_kind == 1 ? (size_t)w : (size_t)wp * 4);
+    const size_t out_img = (size_t)h * wp * 4;
+    cudaStream_t ss[2] = {S(stream0), S(stream1)};
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    // chunk c runs entirely on stream c % 2: H2D -> kernel -> D2H.  In-stream
+    // order protects the reuse of buffer c % 2 by chunk c + 2, and the two
+    // streams let one chunk's H2D overlap the other's kernel and D2H.
+    for (int64_t c = 0, lo = 0; lo < n; ++c, lo += chunk_images) {
+        const int64_t k = (n - lo) < chunk_images ? (n - lo) : chunk_images;
+        const int b = (int)(c & 1);
+        cudaError_t e = cudaMemcpyAsync(dev_in[b], (const char *)host_in + lo * in_img, k * in_img,
+                                        cudaMemcpyHostToDevice, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
+        rc = edges_impl(dev_in[b], input_kind, input_kind == 1 ? w : wp, nullptr, nullptr,
+                        dev_out[b], nullptr, side, nullptr, 32, wp, k, h, w, fill_bit, 0, k * h,
+                        ss[b]);
+        if (rc) return rc;
+        e = cudaMemcpyAsync((char *)host_out + lo * out_img, dev_out[b], k * out_img,
+                            cudaMemcpyDeviceToHost, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "D2H: %s", cudaGetErrorString(e));
+    }
+    if (blocking) {
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaStreamSynchronize(ss[b]);
+            if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+        }
+    }
+    return BE_OK;
+}
+
 }  // extern "C"
