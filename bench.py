@@ -344,7 +344,8 @@ def run_ours(args):
     ins, outs = [base], []
     for _ in range(pool - 1):
         ins.append(base.clone())
-    for _ in range(pool):
+    # at least one output per parallel stream, so overlapping steps never share one
+    for _ in range(max(pool, args.streams)):
         shape = (base.shape[0], base.shape[1], wp)
         outs.append(torch.empty(shape, dtype=torch.int32, device=dev))
 
@@ -359,11 +360,11 @@ def run_ours(args):
         use_graph = False
     else:
         def step(i):
-            j = i % pool
+            x, o = ins[i % len(ins)], outs[i % len(outs)]
             if kind == "u8":
-                cu.pack_edges_u8(ins[j], 1, out=outs[j])
+                cu.pack_edges_u8(x, 1, out=o)
             else:
-                cu.edges_packed(ins[j], w, 1, out=outs[j])
+                cu.edges_packed(x, w, 1, out=o)
         launches_per_step = 1
         use_graph = (step_bytes < (64 << 20)) and not args.no_graph
 
@@ -425,11 +426,38 @@ def run_ours(args):
             torch.cuda.synchronize()
             return a.elapsed_time(b) / n_s
     else:
-        def run(k):
-            for i in range(k):
-                step(i)
+        nst = args.streams if not (shard == "rows" and world > 1) else 1
+        side = [torch.cuda.Stream(dev) for _ in range(max(1, nst))]
 
-        serial_step_ms = None
+        def run(k, nstreams=nst):
+            """Direct launches; independent steps alternate over `nstreams`
+            streams (fork/join around the K steps), as in the graph path."""
+            if nstreams <= 1:
+                for i in range(k):
+                    step(i)
+                return
+            cur = torch.cuda.current_stream(dev)
+            for s_ in side[:nstreams]:
+                s_.wait_stream(cur)
+            for i in range(k):
+                with torch.cuda.stream(side[i % nstreams]):
+                    step(i)
+            for s_ in side[:nstreams]:
+                cur.wait_stream(s_)
+
+        def serial_step_ms():
+            n_s = max(3, min(steps, 20))
+            run(1, 1)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            run(n_s, 1)
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n_s
+
+        if nst <= 1:
+            serial_step_ms = None
 
     # ---- warm-up, then exactly K timed steps (barrier + sync on both sides)
     run(warmup)
@@ -466,7 +494,7 @@ def run_ours(args):
     # average launch duration in the timed region (steps overlap when streams > 1)
     per_launch_ms = ms / steps / launches_per_step
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-    serial_ms = serial_step_ms() if (use_graph and args.streams > 1) else None
+    serial_ms = serial_step_ms() if (serial_step_ms is not None and args.streams > 1) else None
     peak, peak_src = measured_peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -534,9 +562,8 @@ def run_ours(args):
                                     f"({pool * step_bytes / 2**20:.0f} MiB > 3x L2 "
                                     f"{l2 / 2**20:.0f} MiB)" if pool > 1 else
                                     f"step footprint {step_bytes / 2**20:.0f} MiB > L2",
-                       "launch": ("CUDA graph replay, independent batches on "
-                                  f"{args.streams} parallel branches") if use_graph
-                                 else "direct launches"},
+                       "launch": ("CUDA graph replay" if use_graph else "direct launches")
+                                 + f", independent steps on {args.streams} parallel streams"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,

@@ -135,6 +135,20 @@ int be_count_black(const void *in, int64_t *counts, int word_bits, int64_t n, in
 int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
                   int64_t row_stride_words, int fill_bit, void *stream);
 
+/* ---- grayscale input ------------------------------------- */
+
+/* binarize.threshold (sample >= threshold -> white) fused with
+ * detect_edges_mask: uint8 luminance [n][h][in_row_stride] -> edge words; the
+ * binarised raster itself optionally lands in binary_or_null.  threshold = 1 is
+ * exactly be_pack_edge_u8 (nonzero = white). */
+int be_threshold_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                         int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                         int fill_bit, uint32_t *binary_or_null, void *stream);
+/* binarize.threshold alone: uint8 luminance -> packed raster (word_bits 32/64). */
+int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                    void *stream);
+
 /* ---- host buffers (the end-to-end path) ----------------------------------- */
 
 /* Edges of a batch that lives in HOST memory (pinned for overlap): uint8 pixels

@@ -44,6 +44,8 @@ _SIGNATURES = {
     "be_shift_and": [_P, _P, _P, _INT, _I64, _I64, _I64, _I64, _INT, _INT, _P],
     "be_count_black": [_P, _P, _INT, _I64, _I64, _I64, _I64, _P],
     "be_scan_edges": [_P, _P, _INT, _I64, _I64, _I64, _I64, _INT, _P],
+    "be_threshold_edge_u8": [_P, _P, _I64, _I64, _I64, _I64, _I64, _INT, _INT, _P, _P],
+    "be_threshold_u8": [_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _INT, _P],
     "be_host_edges": [_P, _INT, _P, _I64, _I64, _I64, _INT, ctypes.POINTER(_P),
                       ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_last_error": [],

@@ -229,7 +229,7 @@ inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
             const void *below, uint32_t *o_edges, uint32_t *o_eset, int64_t out_stride_u32,
-            const Geometry &G, int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
+            const Geometry &G, int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
     const char *e = getenv("BITEDGE_KERNEL");
     if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return 1;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
@@ -254,6 +254,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                        : 4;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
+    rp.thr = thr;
     const int ocw = input_kind == 1 ? 1 : cw;
     rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
     if (input_kind == 1 && !above && !below && row_lo == 0 && row_hi == nrows &&
@@ -394,7 +395,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
 int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
                const void *below, uint32_t *o_edges, uint32_t *o_eset, int word_bits,
                int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
-               int64_t row_hi, cudaStream_t st) {
+               int64_t row_hi, cudaStream_t st, int thr) {
     if (!stream_allowed()) return 1;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
     if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
@@ -407,6 +408,7 @@ int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void 
     sp.nrows = nrows; sp.h = G.h; sp.w = G.w; sp.row_lo = row_lo; sp.row_hi = row_hi;
     sp.wp = G.wp; sp.pl = G.pl; sp.lastbit = G.lastbit; sp.padmask = G.padmask;
     sp.fillword = G.fillword;
+    sp.thr = thr;
     sp.vst = (out_stride_u32 % 4 == 0) && al16(o_edges) && al16(o_eset);
     int TQ, stage_target = 24 * 1024;
     if (input_kind == 0) {
@@ -450,7 +452,7 @@ int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void 
 int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *above,
                const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
                uint32_t *o_packed, int word_bits, int64_t out_stride_words, int64_t n, int64_t h,
-               int64_t w, int fill_bit, int64_t row_lo, int64_t row_hi, void *stream) {
+               int64_t w, int fill_bit, int64_t row_lo, int64_t row_hi, void *stream, int thr = 1) {
     Geometry G;
     int rc = make_geometry(G, word_bits, n, h, w, fill_bit);
     if (rc) return rc;
@@ -487,6 +489,8 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     tp.nrows = nrows; tp.h = h; tp.w = w; tp.row_lo = row_lo; tp.row_hi = row_hi;
     tp.wp = G.wp; tp.pl = G.pl; tp.lastbit = G.lastbit; tp.padmask = G.padmask;
     tp.fillword = G.fillword; tp.swap = G.swap;
+    if (thr < 0 || thr > 255) return fail(BE_EINVAL, "threshold must be 0..255, got %d", thr);
+    tp.thr = thr;
 
     // tile shape: TQ pixel words (power of two <= 64) x R rows, ~16 KB of
     // packed input or ~32 KB of uint8 input per CTA, smem <= 48 KB.
@@ -512,10 +516,10 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
         tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
         if (only_edges) {
             rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
-                         tp.out_stride, G, nrows, row_lo, row_hi, st);
+                         tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
             if (rc != 1) return rc;
             rc = try_stream(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
-                            word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st);
+                            word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
             if (rc != 1) return rc;
         }
         bool vec = TQ >= 4 && (tp.in_stride % 4) == 0 && ((uintptr_t)in % 16) == 0 &&
@@ -530,10 +534,10 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     tp.in_stride = in_stride;
     if (only_edges && word_bits == 32) {
         rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, tp.out_stride, G, nrows,
-                     row_lo, row_hi, st);
+                     row_lo, row_hi, st, thr);
         if (rc != 1) return rc;
         rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
-                        G, nrows, row_lo, row_hi, st);
+                        G, nrows, row_lo, row_hi, st, thr);
         if (rc != 1) return rc;
     }
     bool vec = (in_stride % 16) == 0 && ((uintptr_t)in % 16) == 0 &&
@@ -885,6 +889,25 @@ int be_scan_edges(const void *in, void *out, int word_bits, int64_t n, int64_t h
     scan_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(
         (const uint32_t *)in, (uint32_t *)out, g, w);
     return cuda_check("scan_kernel");
+}
+
+int be_threshold_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                         int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                         int fill_bit, uint32_t *binary_or_null, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, binary_or_null,
+                      32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream, threshold);
+}
+
+int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                    void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
+                      (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
+                      stream, threshold);
 }
 
 int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,

@@ -46,6 +46,7 @@ struct RegParams {
     int64_t nstrips;
     int vst;                 // 128-bit output stores allowed
     int v8;                  // uint8 rows are 32-B aligned: 256-bit loads
+    int thr;                 // uint8 pack threshold (1 = nonzero is white)
 };
 
 template <int SWAP>
@@ -193,8 +194,8 @@ edge_reg_packed_kernel(const RegParams p) {
 
 // 32 bytes -> one MSB-first word (pixels x0 .. x0+31); bytes beyond the row are garbage
 // and only ever land in padding bits.
-__device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b) {
-    return (pack16(a) << 16) | pack16(b);
+__device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b, const Thr &T) {
+    return (pack16(a, T) << 16) | pack16(b, T);
 }
 
 // 8 bytes that are all 0 or 1 -> 8 bits MSB-first: x*16 + y puts the flags of
@@ -209,13 +210,13 @@ __device__ __forceinline__ uint32_t pack8_01(uint32_t x, uint32_t y) {
 // binarisation produce): one test per 32 bytes skips the per-byte nonzero
 // normalisation; any other byte value takes the general path.  Exact for all
 // inputs (nonzero -> white, bitimage.py:124,133).
-__device__ __forceinline__ uint32_t pack32_any(uint4 a, uint4 b) {
+__device__ __forceinline__ uint32_t pack32_any(uint4 a, uint4 b, const Thr &T) {
     const uint32_t hi = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
-    if (hi == 0u) {
+    if (hi == 0u && T.t == 1u) {
         return (pack8_01(a.x, a.y) << 24) | (pack8_01(a.z, a.w) << 16) |
                (pack8_01(b.x, b.y) << 8) | pack8_01(b.z, b.w);
     }
-    return pack32(a, b);
+    return pack32(a, b, T);
 }
 
 // ld.global.nc.u8 under a predicate, no branch (lanes with p == 0 keep `dflt`).
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kThreads)
 edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
     pdl_wait();
     pdl_trigger();
+    const Thr T = make_thr(p.thr);
     constexpr int WPR = 1 << LWPR;
     constexpr int RPI = 32 >> LWPR;
     const int64_t img = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -263,7 +265,7 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
         if (k < G) ldg_stream_v8(src + 1024 * k, a[k], b[k]);
     uint32_t wd[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) wd[k] = k < G ? pack32(a[k], b[k]) : 0xFFFFFFFFu;
+    for (int k = 0; k < 8; ++k) wd[k] = k < G ? pack32_any(a[k], b[k], T) : 0xFFFFFFFFu;
 
     uint32_t *oe = p.o_edges + img * (int64_t)G * 32 + lane;
     uint32_t *os = p.o_eset + img * (int64_t)G * 32 + lane;
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(kThreads)
 edge_reg_u8_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
+    const Thr T = make_thr(p.thr);
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
@@ -340,12 +343,12 @@ edge_reg_u8_kernel(const RegParams p) {
             if (i >= 1 && i <= RS) {
                 lbit[i - 1] = fw;
                 rbit[i - 1] = 0u;
-                if (ok && need_l) lbit[i - 1] = ptr[-1] != 0 ? 1u : 0u;
-                if (ok && need_r) rbit[i - 1] = ptr[32] != 0 ? 0x80000000u : 0u;
+                if (ok && need_l) lbit[i - 1] = (uint8_t)ptr[-1] >= T.t ? 1u : 0u;
+                if (ok && need_r) rbit[i - 1] = (uint8_t)ptr[32] >= T.t ? 0x80000000u : 0u;
             }
         }
 #pragma unroll
-        for (int i = 0; i < RS + 2; ++i) wd[i] = pack32(ra[i], rb2[i]);
+        for (int i = 0; i < RS + 2; ++i) wd[i] = pack32_any(ra[i], rb2[i], T);
     }
 
     uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(kThreads)
 edge_roll_u8_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
+    const Thr T = make_thr(p.thr);
     static_assert(RSL % Q == 0 && Q >= 4, "strip must be a multiple of the ring");
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -426,12 +430,12 @@ edge_roll_u8_kernel(const RegParams p) {
         }
         ldg_stream_v8(ok ? ptr : safe, ra[slot], rb2[slot]);
         okm = ok ? (okm | (1u << slot)) : (okm & ~(1u << slot));
-        uint32_t e = ldg_u8_if(ok && need_l, ptr - 1, 0u) != 0u ? 1u : 0u;
-        e |= ldg_u8_if(ok && need_r, ptr + 32, 0u) != 0u ? 0x80000000u : 0u;
+        uint32_t e = ldg_u8_if(ok && need_l, ptr - 1, 0u) >= T.t ? 1u : 0u;
+        e |= ldg_u8_if(ok && need_r, ptr + 32, 0u) >= T.t ? 0x80000000u : 0u;
         eb[slot] = e;
     };
     auto word = [&](int slot) -> uint32_t {
-        return (okm >> slot) & 1u ? pack32_any(ra[slot], rb2[slot]) : 0xFFFFFFFFu;
+        return (okm >> slot) & 1u ? pack32_any(ra[slot], rb2[slot], T) : 0xFFFFFFFFu;
     };
 
     uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
@@ -525,6 +529,7 @@ __device__ __forceinline__ void wtma(void *dst, const void *src, uint32_t bytes,
 template <int RSL, int D, int OUT, bool HALO>
 __global__ void __launch_bounds__(kThreads)
 edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
+    const Thr T = make_thr(p.thr);
     constexpr int SLOT = 1056;                       // 16 + 1024 + 16 bytes
     constexpr int WARPS = kThreads / 32;
     extern __shared__ __align__(128) char tsm[];
@@ -598,9 +603,9 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
             const char *src = ring + slot * SLOT + 16 + 32 * lane;
             const uint4 a = *reinterpret_cast<const uint4 *>(src);
             const uint4 b = *reinterpret_cast<const uint4 *>(src + 16);
-            w_new = pack32_any(a, b);
-            if (lane == 0) e_new = src[-1] != 0 ? 1u : 0u;
-            if (lane == 31) e_new = src[32] != 0 ? 0x80000000u : 0u;
+            w_new = pack32_any(a, b, T);
+            if (lane == 0) e_new = (uint8_t)src[-1] >= T.t ? 1u : 0u;
+            if (lane == 31) e_new = (uint8_t)src[32] >= T.t ? 0x80000000u : 0u;
         }
         // slot i % D is free (consumed, or never filled because staged row i does
         // not exist): refill it with staged row i + D
@@ -642,6 +647,7 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
 template <int RSL, int D, int OUT, bool HALO>
 __global__ void __launch_bounds__(kThreads)
 edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
+    const Thr T = make_thr(p.thr);
     constexpr int SEG = 2048;                        // pixels (bytes) per warp segment
     constexpr int SLOT = 16 + SEG + 16;
     constexpr int WARPS = kThreads / 32;
@@ -714,11 +720,11 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
             phase ^= 1u << slot;
             const char *s = ring + slot * SLOT + 16;
             na = pack32_any(*reinterpret_cast<const uint4 *>(s + 32 * lane),
-                            *reinterpret_cast<const uint4 *>(s + 32 * lane + 16));
+                            *reinterpret_cast<const uint4 *>(s + 32 * lane + 16), T);
             nb = pack32_any(*reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane),
-                            *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16));
-            if (lane == 0) nel = s[-1] != 0 ? 1u : 0u;
-            if (lane == 31) ner = s[SEG] != 0 ? 0x80000000u : 0u;
+                            *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16), T);
+            if (lane == 0) nel = (uint8_t)s[-1] >= T.t ? 1u : 0u;
+            if (lane == 31) ner = (uint8_t)s[SEG] >= T.t ? 0x80000000u : 0u;
         }
         __syncwarp();
         if (lane == 0) issue(i + D);                 // slot free (consumed or unused)

@@ -54,6 +54,7 @@ struct StreamParams {
     int stage_bytes;         // raw bytes per stage (multiple of 16)
     int stages;
     int pieces;              // uint8: 16-byte pieces of a staged row that lie in the row
+    int thr;                 // uint8 pack threshold (1 = nonzero is white)
     int vst;                 // outputs allow 128-bit stores (16-B aligned rows)
 };
 
@@ -203,6 +204,7 @@ edge_stream_kernel(const StreamParams p) {
     uint32_t *pk = reinterpret_cast<uint32_t *>(bars + S);
     const int PP = TQ + 8;
     const int tid = threadIdx.x;
+    const Thr T = make_thr(p.thr);
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -254,9 +256,9 @@ edge_stream_kernel(const StreamParams p) {
                 uint32_t word = 0xFFFFFFFFu;               // words past the staged row
                 if (2 * jw < p.pieces) {
                     const char *src = st + i * p.raw_pitch + p.col0 + 32 * jw;
-                    const uint32_t hi = pack16(*reinterpret_cast<const uint4 *>(src));
+                    const uint32_t hi = pack16(*reinterpret_cast<const uint4 *>(src), T);
                     const uint32_t lo = 2 * jw + 1 < p.pieces
-                                            ? pack16(*reinterpret_cast<const uint4 *>(src + 16))
+                                            ? pack16(*reinterpret_cast<const uint4 *>(src + 16), T)
                                             : 0xFFFFu;
                     word = (hi << 16) | lo;
                 }
@@ -266,7 +268,7 @@ edge_stream_kernel(const StreamParams p) {
                 for (int idx = tid; idx < 2 * (R + 2); idx += kThreads) {
                     const int i = idx >> 1, right = idx & 1;
                     const uint32_t half = pack16(*reinterpret_cast<const uint4 *>(
-                        st + i * p.raw_pitch + p.col0 + (right ? 32 * TQ : -16)));
+                        st + i * p.raw_pitch + p.col0 + (right ? 32 * TQ : -16)), T);
                     pk[i * PP + (right ? TQ + 4 : 3)] = right ? (half << 16) : half;
                 }
             }

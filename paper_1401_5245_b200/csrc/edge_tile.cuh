@@ -67,6 +67,7 @@ struct TileParams {
     int swap;              // 1 for uint64 storage
     int log_tq, log_r;     // tile = (1<<log_r) rows x (1<<log_tq) words
     int tiles_x;
+    int thr;               // uint8 pack: white iff sample >= thr (1 = from_array)
 };
 
 __device__ __forceinline__ uint4 ldg_stream_v4(const void *p) {
@@ -87,33 +88,55 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Nonzero-byte flags: bit 7 of each byte set iff the byte is nonzero.
-__device__ __forceinline__ uint32_t nz_bytes(uint32_t v) {
-    return (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
+// Pixel rule of the uint8 -> bit pack: white iff sample >= t.  t = 1 is
+// BitImage.from_array's "nonzero = white" (bitimage.py:124,133); any other t is
+// binarize.threshold ("sample >= t -> White"), fused into the
+// edge kernels as SURVEY 8(f) F2.
+struct Thr {
+    uint32_t t;     // threshold 0..255
+    uint32_t tl;    // (t & 0x7f) replicated into every byte
+    uint32_t m;     // ~0 when t < 128, else 0
+};
+
+__device__ __forceinline__ Thr make_thr(int t) {
+    Thr T;
+    T.t = (uint32_t)t;
+    T.tl = ((uint32_t)t & 0x7Fu) * 0x01010101u;
+    T.m = t < 128 ? 0xFFFFFFFFu : 0u;
+    return T;
+}
+
+// Bit 7 of each byte set iff byte >= t: with b = 128*bh + bl, bl >= tl is the
+// no-borrow bit of ((bl | 0x80) - tl); then ge = bh | that (t < 128) or
+// bh & that (t >= 128), one LOP3 either way.  For t = 1 this is "byte != 0".
+__device__ __forceinline__ uint32_t ge_bytes(uint32_t v, const Thr &T) {
+    const uint32_t x = ((v & 0x7F7F7F7Fu) | 0x80808080u) - T.tl;
+    return ((v & x) | (T.m & (v | x))) & 0x80808080u;
 }
 
 // 8 bytes (a = pixels 0..3, b = pixels 4..7, little-endian: pixel 0 is the low
 // byte) -> 8 bits MSB-first.  The flags of `a` sit at bits 4,12,20,28 and of
 // `b` at 0,8,16,24; one 32x32->64 multiply by 2^31+2^22+2^13+2^4 moves them to
 // bits 35..28 in pixel order with no two partial products colliding.
-__device__ __forceinline__ uint32_t pack8(uint32_t a, uint32_t b) {
-    uint32_t t = (nz_bytes(a) >> 3) | (nz_bytes(b) >> 7);
+__device__ __forceinline__ uint32_t pack8(uint32_t a, uint32_t b, const Thr &T) {
+    uint32_t t = (ge_bytes(a, T) >> 3) | (ge_bytes(b, T) >> 7);
     uint64_t prod = (uint64_t)t * 0x80402010ull;
     return (uint32_t)(prod >> 28) & 0xFFu;
 }
 
-__device__ __forceinline__ uint32_t pack16(uint4 v) {
-    return (pack8(v.x, v.y) << 8) | pack8(v.z, v.w);
+__device__ __forceinline__ uint32_t pack16(uint4 v, const Thr &T) {
+    return (pack8(v.x, v.y, T) << 8) | pack8(v.z, v.w, T);
 }
 
 // Byte-wise pack of pixels [x0, x0+16) of a row, pixels >= w read as white.
-__device__ __forceinline__ uint32_t pack16_bytes(const uint8_t *row, int64_t x0, int64_t w) {
+__device__ __forceinline__ uint32_t pack16_bytes(const uint8_t *row, int64_t x0, int64_t w,
+                                                 const Thr &T) {
     uint32_t v = 0;
 #pragma unroll
     for (int b = 0; b < 16; ++b) {
         int64_t x = x0 + b;
         uint32_t bit = 1u;
-        if (x < w) bit = row[x] != 0;
+        if (x < w) bit = row[x] >= T.t;
         v = (v << 1) | bit;
     }
     return v;
@@ -147,8 +170,9 @@ __device__ __forceinline__ void stage_item(uint32_t *srow, const char *row, int 
     } else {
         uint32_t half = 0xFFFFu;
         if (row != nullptr && x0 < p.w) {
-            if (KIND == kU8Vec && x0 + 16 <= p.w) half = pack16(ldg_stream_v4(row + x0));
-            else half = pack16_bytes((const uint8_t *)row, x0, p.w);
+            const Thr T = make_thr(p.thr);
+            if (KIND == kU8Vec && x0 + 16 <= p.w) half = pack16(ldg_stream_v4(row + x0), T);
+            else half = pack16_bytes((const uint8_t *)row, x0, p.w, T);
         }
         reinterpret_cast<uint16_t *>(srow)[2 * (c >> 1) + ((c & 1) ? 0 : 1)] = (uint16_t)half;
     }
@@ -158,6 +182,7 @@ template <int KIND, int OUT>
 __global__ void __launch_bounds__(kThreads)
 edge_tile_kernel(const TileParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
+    const Thr T = make_thr(p.thr);
     constexpr bool U8 = (KIND == kU8Vec || KIND == kU8Byte);
     const int log_tq = p.log_tq;
     const int TQ = 1 << log_tq;
@@ -220,9 +245,9 @@ edge_tile_kernel(const TileParams p) {
                         uint32_t *srow = smem + (r + 1) * P + 4;
                         if (U8) {
                             uint32_t half = 0xFFFFu;
-                            if (full[u]) half = pack16(v[u]);
+                            if (full[u]) half = pack16(v[u], T);
                             else if (row_at(r) != nullptr && x0 < p.w)
-                                half = pack16_bytes((const uint8_t *)row_at(r), x0, p.w);
+                                half = pack16_bytes((const uint8_t *)row_at(r), x0, p.w, T);
                             reinterpret_cast<uint16_t *>(srow)[2 * (c >> 1) + ((c & 1) ? 0 : 1)] =
                                 (uint16_t)half;
                         } else {
@@ -263,7 +288,7 @@ edge_tile_kernel(const TileParams p) {
                 } else {
                     const int64_t hx = (int64_t)pw * 32 + (right ? 0 : 16);
                     if (hx < p.w) {
-                        const uint32_t half = pack16_bytes((const uint8_t *)row, hx, p.w);
+                        const uint32_t half = pack16_bytes((const uint8_t *)row, hx, p.w, T);
                         v = right ? (half << 16) : half;
                     }
                 }

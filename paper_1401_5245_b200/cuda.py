@@ -169,6 +169,50 @@ def pack_edges_u8(pixels: torch.Tensor, border=WHITE_OUTSIDE, *, out=None,
     return o[0] if (squeeze and out is None) else o
 
 
+def threshold_edges_u8(gray: torch.Tensor, threshold: int, border=WHITE_OUTSIDE, *, out=None,
+                       binary_out: torch.Tensor | None = None) -> torch.Tensor:
+    """binarize.threshold (SPEC.md:237-245, sample >= t -> white) fused with
+    detect_edges_mask: uint8 luminance [N,H,W] -> int32 edge words, one pass
+    (SURVEY 8(f) F2).  `binary_out` additionally receives the binarised raster."""
+    t = int(threshold)
+    if not 0 <= t <= 255:
+        raise ValueError(f"threshold must be 0..255, got {threshold}")
+    squeeze = gray.dim() == 2
+    p3, prs = _pixels(gray, "gray")
+    if p3.dtype != torch.uint8:
+        raise ValueError("gray must be uint8 luminance")
+    n, h, w = p3.shape
+    shape = (n, h, words_per_row(w, 32))
+    o = out if out is not None else torch.empty(shape, dtype=torch.int32, device=p3.device)
+    o3 = _as3d(o, "out")
+    if tuple(o3.shape) != shape or word_bits_of(o3) != 32:
+        raise ValueError(f"out must be 32-bit words of shape {shape}")
+    ors = _row_stride(o3, "out")
+    bo = None
+    if binary_out is not None:
+        bo = _as3d(binary_out, "binary_out")
+        if tuple(bo.shape) != shape or word_bits_of(bo) != 32 or _row_stride(bo, "binary_out") != ors:
+            raise ValueError("binary_out must match out")
+    _capi.call("be_threshold_edge_u8", _ptr(p3), _ptr(o3), n, h, w, prs, ors, t, fill_bit(border),
+               _ptr(bo), ctypes.c_void_p(_stream(p3)))
+    return o[0] if (squeeze and out is None) else o
+
+
+def threshold_u8(gray: torch.Tensor, threshold: int, word_bits: int = 32) -> torch.Tensor:
+    """binarize.threshold on the device: packed raster."""
+    t = int(threshold)
+    if not 0 <= t <= 255:
+        raise ValueError(f"threshold must be 0..255, got {threshold}")
+    squeeze = gray.dim() == 2
+    p3, prs = _pixels(gray, "gray")
+    n, h, w = p3.shape
+    shape = (n, h, words_per_row(w, word_bits))
+    o = torch.empty(shape, dtype=torch.int64 if word_bits == 64 else torch.int32, device=p3.device)
+    _capi.call("be_threshold_u8", _ptr(p3), _ptr(o), word_bits, n, h, w, prs,
+               _row_stride(o, "out"), t, ctypes.c_void_p(_stream(p3)))
+    return o[0] if squeeze else o
+
+
 def edges_general(inp: torch.Tensor, width: int | None = None, border=WHITE_OUTSIDE, *,
                   word_bits: int = 32, edges=True, edgeset=False, sides=False, packed=False,
                   above=None, below=None, row_lo: int = 0, row_hi: int | None = None,

@@ -374,3 +374,35 @@ def test_fill_policies_on_border_touching_figure(cuda_dev):
     b = P.unpack_u32(_u32(cu.pack_edges_u8(t, 0)), 70)[0]
     assert (w[2:-2, 2:-2] == b[2:-2, 2:-2]).all()
     assert (w[0] == 0).all() and (b[0] == 1).all()
+
+
+# ---------------------------------------------------------------- F2: threshold fused into the pack
+
+@pytest.mark.parametrize("t", [0, 1, 2, 77, 127, 128, 129, 200, 255])
+def test_threshold_edges_fused(cuda_dev, t):
+    """binarize.threshold (sample >= t -> white, SPEC.md:237-245) + edges in one
+    kernel == threshold on the host followed by the oracle scan."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(t)
+    for (n, h, w) in [(3, 45, 2048), (2, 33, 100), (64, 64, 64), (1, 1, 7)]:
+        g = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+        binary = (g >= t).astype(np.uint8)
+        exp = cscan.scan_u8(binary, 1)
+        bo = torch_empty_like_words(_t(g, cuda_dev))
+        got = _u32(cu.threshold_edges_u8(_t(g, cuda_dev), t, 1, binary_out=bo))
+        assert (got == exp).all(), (t, n, h, w)
+        assert (_u32(bo) == P.pack_u32(binary)).all(), (t, n, h, w)
+        assert (_u32(cu.threshold_u8(_t(g, cuda_dev), t)) == P.pack_u32(binary)).all()
+
+
+def test_threshold_spec_examples(cuda_dev):
+    from paper_1401_5245_b200.binarize import threshold, threshold_edges
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    g = np.array([[0, 127, 128, 255]], dtype=np.uint8)
+    assert threshold(g, 128).to_array().tolist() == [[0, 0, 1, 1]]          # SPEC:243
+    assert threshold(g, 0).to_array().tolist() == [[1, 1, 1, 1]]            # SPEC:244
+    assert threshold(np.full((2, 3), 254, np.uint8), 255).count_black() == 6  # SPEC:245
+    b, e = threshold_edges(g, 128)
+    assert e == detect_edges_mask(b)

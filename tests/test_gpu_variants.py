@@ -96,3 +96,15 @@ def test_row_slabs_each_variant(variant, cuda_dev):
         below = pk[hi].clone() if hi < H else None
         parts.append(cu.edges_halo(slab, above, below, W, 1))
     assert torch.equal(torch.cat(parts), whole), variant
+
+
+@pytest.mark.parametrize("t", [1, 100, 200])
+def test_threshold_each_variant(variant, t, cuda_dev):
+    """F2 (threshold fused into the pack) through every kernel variant."""
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(t)
+    for (n, h, w) in [(16, 64, 64), (2, 40, 2048), (3, 21, 333), (1, 70, 4096)]:
+        g = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+        exp = cscan.scan_u8((g >= t).astype(np.uint8), 1)
+        assert (_u32(cu.threshold_edges_u8(_t(g, cuda_dev), t, 1)) == exp).all(), (variant, t, w)
