@@ -149,6 +149,22 @@ int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int6
                     int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
                     void *stream);
 
+/* ---- PBM P4 at the kernel boundary ----------------------- */
+
+/* The P4 payload: rows of ceil(w/8) bytes, MSB-first, 1 = black.
+ * decode: P4 -> packed raster (1 = white, padding 1; word_bits 32 or 64);
+ * encode: packed raster -> P4 (padding bits written 0). */
+int be_p4_decode(const uint8_t *p4, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                 int64_t out_row_stride_words, void *stream);
+int be_p4_encode(const void *in, uint8_t *p4, int word_bits, int64_t n, int64_t h, int64_t w,
+                 int64_t in_row_stride_words, void *stream);
+/* detect_edges_mask from a P4 payload to a P4 payload.  When a P4 row is a whole
+ * number of 16-byte chunks (w % 128 in 121..128 or 0) kernel K1 reads and writes
+ * P4 directly (byte swap + inversion in registers, 0.25 B/px); otherwise it runs
+ * decode -> K1 -> encode through `scratch_or_null` (2 * n * h * ceil(w/32) words). */
+int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int64_t h, int64_t w,
+                int fill_bit, uint32_t *scratch_or_null, void *stream);
+
 /* ---- host buffers (the end-to-end path) ----------------------------------- */
 
 /* Edges of a batch that lives in HOST memory (pinned for overlap): uint8 pixels

@@ -46,6 +46,9 @@ _SIGNATURES = {
     "be_scan_edges": [_P, _P, _INT, _I64, _I64, _I64, _I64, _INT, _P],
     "be_threshold_edge_u8": [_P, _P, _I64, _I64, _I64, _I64, _I64, _INT, _INT, _P, _P],
     "be_threshold_u8": [_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _INT, _P],
+    "be_p4_decode": [_P, _P, _INT, _I64, _I64, _I64, _I64, _P],
+    "be_p4_encode": [_P, _P, _INT, _I64, _I64, _I64, _I64, _P],
+    "be_p4_edges": [_P, _P, _I64, _I64, _I64, _INT, _P, _P],
     "be_host_edges": [_P, _INT, _P, _I64, _I64, _I64, _INT, ctypes.POINTER(_P),
                       ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_last_error": [],

@@ -92,7 +92,11 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
 
 // Item = CW pixel words of one row (memory order == pixel order for uint32 rows;
 // uint64 rows swap the halves of each word pair).  RS rows per strip.
-template <int SWAP, int RS, int CW, int OUT, bool HALO>
+// PBM P4 rows (1 = black, MSB-first bytes) <-> pixel-order words (1 = white):
+// byte-swap the little-endian load and invert.
+__device__ __forceinline__ uint32_t p4_word(uint32_t v) { return ~__byte_perm(v, 0, 0x0123); }
+
+template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false>
 __global__ void __launch_bounds__(kThreads)
 edge_reg_packed_kernel(const RegParams p) {
     pdl_wait();
@@ -125,6 +129,10 @@ edge_reg_packed_kernel(const RegParams p) {
         }
         if (ok) {
             load_chunk<CW>(ptr, v[i]);
+            if (P4) {
+#pragma unroll
+                for (int q = 0; q < CW; ++q) v[i][q] = p4_word(v[i][q]);
+            }
         } else {
 #pragma unroll
             for (int q = 0; q < CW; ++q) v[i][q] = fw;
@@ -134,6 +142,10 @@ edge_reg_packed_kernel(const RegParams p) {
             rwx[i - 1] = 0u;
             if (ok && need_l) lwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? -2 : -1));
             if (ok && need_r) rwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? CW + 1 : CW));
+            if (P4) {
+                if (ok && need_l) lwx[i - 1] = p4_word(lwx[i - 1]);
+                if (ok && need_r) rwx[i - 1] = p4_word(rwx[i - 1]);
+            }
         }
     }
 
@@ -172,7 +184,7 @@ edge_reg_packed_kernel(const RegParams p) {
                 const uint32_t u = top ? fw : cu[q];
                 const uint32_t d = bot ? fw : cd[q];
                 const uint32_t a = ln | rn | u | d;
-                ve[q ^ SWAP] = cc[q] | ~a | f;
+                ve[q ^ SWAP] = P4 ? p4_word(cc[q] | ~a | f) : (cc[q] | ~a | f);
                 vs[q ^ SWAP] = (~cc[q] & a) | f;
             }
             if (nst == CW && p.vst) {

@@ -406,3 +406,48 @@ def test_threshold_spec_examples(cuda_dev):
     assert threshold(np.full((2, 3), 254, np.uint8), 255).count_black() == 6
     b, e = threshold_edges(g, 128)
     assert e == detect_edges_mask(b)
+
+
+# ---------------------------------------------------------------- F1: PBM P4 at the kernel boundary
+
+def test_pbm_spec_examples(cuda_dev):
+    from paper_1401_5245_b200.pbm import read_pbm, write_pbm
+
+    assert read_pbm(b"P1\n3 1\n1 0 1\n").to_array().tolist() == [[0, 1, 0]]
+    assert read_pbm(b"P4\n3 1\n\xa0").to_array().tolist() == [[0, 1, 0]]
+    f = b"P4\n3 1\n\xa0"
+    assert write_pbm(read_pbm(f), raw=True) == f
+    with pytest.raises(ValueError, match="offset"):
+        read_pbm(b"P4\n16 2\n\x00\x00\x00")                                  # short payload
+
+
+def test_pbm_roundtrip_and_detect(cuda_dev):
+    """read∘write identity on random rasters (acceptance 8) and the
+    fused P4 -> edges -> P4 path against the oracle, aligned and unaligned rows."""
+    from paper_1401_5245_b200.bitimage import BitImage
+    from paper_1401_5245_b200.pbm import detect_pbm, read_pbm, write_pbm
+
+    rng = np.random.default_rng(4)
+    for (h, w) in [(5, 3), (17, 100), (9, 128), (33, 1024), (3, 250), (64, 2048), (2, 8192), (7, 1)]:
+        a = (rng.random((h, w)) < 0.5).astype(np.uint8)
+        img = BitImage.from_array(a)
+        for raw in (True, False):
+            data = write_pbm(img, raw)
+            assert read_pbm(data) == img, (h, w, raw)
+        p4 = write_pbm(img, True)
+        exp = P.to_array(P.detect_edges_mask(P.from_array(a), 1))
+        for unfused in (False, True):
+            import os
+
+            if unfused:
+                os.environ["BITEDGE_P4_UNFUSED"] = "1"
+            try:
+                got = read_pbm(detect_pbm(p4)).to_array()
+            finally:
+                os.environ.pop("BITEDGE_P4_UNFUSED", None)
+            assert (got == exp).all(), (h, w, unfused)
+        # P4 padding bits of the output are zero (SPEC:304)
+        if w % 8:
+            out = detect_pbm(p4)
+            payload = np.frombuffer(out[-((w + 7) // 8) * h:], np.uint8).reshape(h, -1)
+            assert not (payload[:, -1] & ((1 << (8 - w % 8)) - 1)).any()

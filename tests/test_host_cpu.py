@@ -206,3 +206,19 @@ def test_c4_slab_rasteriser_matches_bruteforce():
     assert (got == P.pack_u32(ref)).all()
     part = synth.c4_slab(100, 300, disks, size=size).numpy().view(np.uint32)
     assert (part == got[100:300]).all()
+
+
+# ---------------------------------------------------------------- PBM header (F1 host side)
+
+def test_pbm_header_parsing():
+    from paper_1401_5245_b200.pbm import parse_header
+
+    assert parse_header(b"P1\n3 1\n1 0 1\n") == ("P1", 3, 1, 7)
+    assert parse_header(b"P4\n3 1\n\xa0") == ("P4", 3, 1, 7)
+    assert parse_header(b"P4 # comment\n  12\t7\n") == ("P4", 12, 7, 20)
+    with pytest.raises(ValueError, match="offset 0"):
+        parse_header(b"P5\n1 1\n")
+    with pytest.raises(ValueError, match="offset"):
+        parse_header(b"P4\n3 \n")
+    with pytest.raises(ValueError, match="at least 1x1"):
+        parse_header(b"P4\n0 3\n")
