@@ -160,12 +160,10 @@ bool stream_allowed() {
 
 template <int KIND, int OUT>
 int launch_stream_out(StreamParams &sp, size_t smem, cudaStream_t st) {
-    thread_local size_t attr_set = 0;
-    if (smem > 48 * 1024 && smem > attr_set) {
+    if (smem > 48 * 1024) {   // per launch: the attribute is per device
         cudaError_t e = cudaFuncSetAttribute(edge_stream_kernel<KIND, OUT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return fail((int)e, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        attr_set = smem;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_stream_kernel<KIND, OUT>, kThreads,
@@ -304,11 +302,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
 #define BE_TMA2(OUTK, H)                                                                        \
     do {                                                                                        \
         auto kern = edge_tma2_u8_kernel<kRSLT, kD, OUTK, H>;                                    \
-        thread_local bool attr = false;                                                         \
-        if (!attr) {                                                                            \
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            attr = true;                                                                        \
-        }                                                                                       \
+        /* per launch: the attribute is per device, and these launches are long */             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
     } while (0)
             if (rp.o_edges && rp.o_eset) {
@@ -336,11 +331,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
 #define BE_TMA(OUTK, H)                                                                         \
     do {                                                                                        \
         auto kern = edge_tma_u8_kernel<kRSLT, kD, OUTK, H>;                                     \
-        thread_local bool attr = false;                                                         \
-        if (!attr) {                                                                            \
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            attr = true;                                                                        \
-        }                                                                                       \
+        /* per launch: the attribute is per device, and these launches are long */             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
     } while (0)
             if (rp.o_edges && rp.o_eset) {

@@ -13,8 +13,9 @@ from paper_1401_5245_b200 import cuda as cu  # noqa: E402
 
 SHAPES = {"c1": ("u8", 1, 256, 256), "c2": ("u8", 4096, 64, 64), "c3": ("packed", 1, 8192, 8192),
           "c4": ("packed", 1, 65536, 65536), "c5": ("u8", 1024, 2048, 2048),
-          "c3_64": ("packed64", 1, 8192, 8192)}
-BPP = {"u8": 1.125, "packed": 0.25, "packed64": 0.25}
+          "c3_64": ("packed64", 1, 8192, 8192), "c3_p4": ("p4", 1, 8192, 8192),
+          "c4_p4": ("p4", 1, 65536, 65536)}
+BPP = {"u8": 1.125, "packed": 0.25, "packed64": 0.25, "p4": 0.25}
 
 
 def run(cfg, iters=200):
@@ -26,6 +27,9 @@ def run(cfg, iters=200):
         in_b, out_b = n * h * w, n * h * outw * 4
     elif kind == "packed":
         base = torch.randint(-2**31, 2**31 - 1, (n, h, w // 32), dtype=torch.int32, device=dev)
+        in_b = out_b = n * h * w // 8
+    elif kind == "p4":
+        base = torch.randint(0, 256, (n * h * (w // 8),), dtype=torch.uint8, device=dev)
         in_b = out_b = n * h * w // 8
     else:
         base = torch.randint(-2**62, 2**62, (n, h, w // 64), dtype=torch.int64, device=dev)
@@ -40,10 +44,14 @@ def run(cfg, iters=200):
         else:
             outs.append(torch.empty_like(x))
 
+    from paper_1401_5245_b200 import pbm
+
     def step(i):
         j = i % pool
         if kind == "u8":
             cu.pack_edges_u8(ins[j], 1, out=outs[j])
+        elif kind == "p4":
+            outs[j] = pbm.detect_p4(ins[j], n, h, w)
         else:
             cu.edges_packed(ins[j], w, 1, out=outs[j])
 
