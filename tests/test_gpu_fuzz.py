@@ -1,0 +1,99 @@
+"""Seeded fuzzing of the whole dispatch surface against the per-pixel C oracle:
+random batch shapes (including 1-pixel rows/columns), row-stride padding,
+byte offsets that break alignment, border policy, threshold, uint8 / packed
+u32 / packed u64 / P4 inputs and every kernel-selection knob.  Bit-exact."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cscan
+from oracle import port as P
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = [{}, {"BITEDGE_KERNEL": "tile"}, {"BITEDGE_KERNEL": "stream"}, {"BITEDGE_CW4": "1"},
+         {"BITEDGE_NO_ROLL": "1"}, {"BITEDGE_NO_WARPIMG": "1"}, {"BITEDGE_FORCE_TMA": "1"},
+         {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA1": "1"}, {"BITEDGE_PDL": "0"},
+         {"BITEDGE_RS": "8"}]
+
+
+def _shape(rng):
+    kind = rng.integers(0, 5)
+    if kind == 0:
+        return int(rng.integers(1, 9)), int(rng.integers(1, 70)), int(rng.integers(1, 200))
+    if kind == 1:
+        return int(rng.integers(1, 40)), 64, 64
+    if kind == 2:
+        return 1, int(rng.integers(1, 130)), int(rng.choice([1024, 1056, 2048, 2080, 4096, 3000]))
+    if kind == 3:
+        return int(rng.integers(1, 4)), int(rng.integers(1, 5)), int(rng.integers(1, 9000))
+    return int(rng.integers(1, 300)), 1, int(rng.integers(1, 70))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz(seed, cuda_dev, monkeypatch):
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(1000 + seed)
+    for knob in KNOBS:
+        for k, v in knob.items():
+            monkeypatch.setenv(k, v)
+        for _ in range(3):
+            n, h, w = _shape(rng)
+            fill = int(rng.integers(0, 2))
+            t = int(rng.choice([1, 1, 1, 0, 2, 100, 128, 255]))
+            g = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+            g[rng.random((n, h, w)) < 0.4] = 0
+            binary = (g >= t).astype(np.uint8)
+            exp = cscan.scan_u8(binary, fill)
+            # uint8 input, padded row stride and a byte offset that may break alignment
+            pad, off = int(rng.integers(0, 40)), int(rng.integers(0, 3))
+            buf = torch.zeros(n * h * (w + pad) + off + 64, dtype=torch.uint8, device=cuda_dev)
+            view = buf[off:off + n * h * (w + pad)].view(n, h, w + pad)[..., :w]
+            view.copy_(torch.from_numpy(g).to(cuda_dev))
+            got = cu.threshold_edges_u8(view, t, fill).cpu().numpy().view(np.uint32)
+            assert (got == exp).all(), (knob, n, h, w, pad, off, fill, t)
+            # packed u32 with stride padding; packed u64 through the drop-in layout
+            pk = P.pack_u32(binary)
+            spad = int(rng.integers(0, 6))
+            wb = torch.full((n, h, pk.shape[2] + spad), -1, dtype=torch.int32, device=cuda_dev)
+            wb[..., : pk.shape[2]] = torch.from_numpy(pk.view(np.int32)).to(cuda_dev)
+            got32 = cu.edges_packed(wb[..., : pk.shape[2]], w, fill).cpu().numpy().view(np.uint32)
+            assert (got32 == exp).all(), (knob, n, h, w, spad, "u32")
+            w64 = np.stack([P.from_array(x).words for x in binary]).view(np.int64)
+            o64 = cu.edges_packed(torch.from_numpy(w64).to(cuda_dev), w, fill)
+            e64 = np.stack([P.detect_edges_mask(P.from_array(x), fill).words for x in binary])
+            assert (o64.cpu().numpy().view(np.uint64) == e64).all(), (knob, n, h, w, "u64")
+        for k in knob:
+            monkeypatch.delenv(k, raising=False)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_p4(seed, cuda_dev):
+    import torch
+
+    from paper_1401_5245_b200 import pbm
+
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(8):
+        n = int(rng.integers(1, 4))
+        h = int(rng.integers(1, 50))
+        w = int(rng.choice([int(rng.integers(1, 300)), 128, 1024, 2040, 4096]))
+        fill = int(rng.integers(0, 2))
+        a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
+        rb = (w + 7) // 8
+        bits = np.ones((n, h, rb * 8), np.uint8)
+        bits[..., :w] = a
+        payload = np.packbits(1 - bits, axis=-1)                     # P4: 1 = black
+        out = pbm.detect_p4(torch.from_numpy(payload.reshape(-1).copy()).to(cuda_dev), n, h, w,
+                            fill).cpu().numpy().reshape(n, h, rb)
+        got = 1 - np.unpackbits(out, axis=-1)[..., :w]
+        exp = P.unpack_u32(cscan.scan_u8(a, fill), w)
+        assert (got == exp).all(), (n, h, w, fill)
+        if w % 8:
+            assert not (out[..., -1] & ((1 << (8 - w % 8)) - 1)).any()
+        os.environ.pop("BITEDGE_P4_UNFUSED", None)
