@@ -186,8 +186,14 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 
 // Launch helpers: dispatch the runtime choices onto template parameters.
 template <int OUT, bool HALO>
-int launch_reg_packed(RegParams &rp, int swap, int cw, unsigned grid, cudaStream_t st) {
-    if (swap) {
+int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
+    if (!swap && rs == 2) {
+        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
+        else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
+    } else if (!swap && rs == 8) {
+        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp);
+        else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp);
+    } else if (swap) {
         if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
         else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
     } else {
@@ -217,9 +223,9 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
         if (rp.o_eset) return launch_reg_u8<kOutEset, HALO>(rp, rs, grid, st);
         return launch_reg_u8<kOutEdges, HALO>(rp, rs, grid, st);
     }
-    if (rp.o_edges && rp.o_eset) return launch_reg_packed<kOutAny, HALO>(rp, swap, cw, grid, st);
-    if (rp.o_eset) return launch_reg_packed<kOutEset, HALO>(rp, swap, cw, grid, st);
-    return launch_reg_packed<kOutEdges, HALO>(rp, swap, cw, grid, st);
+    if (rp.o_edges && rp.o_eset) return launch_reg_packed<kOutAny, HALO>(rp, swap, cw, rs, grid, st);
+    if (rp.o_eset) return launch_reg_packed<kOutEset, HALO>(rp, swap, cw, rs, grid, st);
+    return launch_reg_packed<kOutEdges, HALO>(rp, swap, cw, rs, grid, st);
 }
 
 // Returns 1 when the register-direct kernel does not apply (caller falls back).
@@ -244,12 +250,15 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
     const bool in32 = al(in, 32) && in_row_bytes % 32 == 0 && al(above, 32) && al(below, 32);
     // packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4
-    // (only when that still gives >= 4 waves of threads; small rasters want more threads)
+    // Packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4.
+    // Small rasters (< 4 waves of 4-row strips) use 2-row strips instead, which
+    // doubles the threads in flight (C3: 5.1 us serial / 88 % overlapped vs
+    // 5.3 / 79 % for 4-word x 4-row items; scripts/c3sweep.sh).
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
-    const int cw = (input_kind == 0 && in32 && !getenv("BITEDGE_CW4") &&
-                    strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096)
-                       ? 8
-                       : 4;
+    const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
+    int cw = (input_kind == 0 && in32 && !getenv("BITEDGE_CW4")) ? 8 : 4;
+    const int packed_rs = (input_kind == 0 && !G.swap && !big) ? 2 : 4;
+    if (input_kind == 0 && in32 && getenv("BITEDGE_CW8")) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
     rp.thr = thr;
@@ -369,10 +378,13 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         }
     }
     // strip height: 4 rows (the one-shot kernels keep every row of the strip in flight)
-    int rs = 4;
+    int rs = input_kind == 0 ? packed_rs : 4;
     if (input_kind == 1) {
         const char *rse = getenv("BITEDGE_RS");
         if (rse) rs = atoi(rse) == 8 ? 8 : 4;
+    } else if (!G.swap) {
+        const char *rse = getenv("BITEDGE_PRS");      // packed strip height experiments: 2/4/8
+        if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
     }
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
