@@ -349,14 +349,26 @@ def run_ours(args):
         shape = (base.shape[0], base.shape[1], wp)
         outs.append(torch.empty(shape, dtype=torch.int32, device=dev))
 
+    halo_mode = None
     if shard == "rows" and world > 1:
-        slabs = [bd.RowShardedEdges(x[0], w, 1) for x in ins]
-        for s, o in zip(slabs, outs):
-            s.out = o[0]
+        slabs = None
+        if args.halo == "p2p":
+            # halo rows read from the neighbours' slabs over NVLink inside the kernel
+            try:
+                slabs = [bd.PeerHaloEdges(x[0], w, 1) for x in ins]
+                halo_mode, launches_per_step = "p2p (CUDA IPC peer reads in the edge kernel)", 1
+            except Exception as e:   # e.g. IPC unavailable in the container
+                log(f"[rank {rank}] p2p halos unavailable ({e}); using NCCL")
+                slabs = None
+        if slabs is None:
+            slabs = [bd.RowShardedEdges(x[0], w, 1) for x in ins]
+            halo_mode, launches_per_step = "nccl (batch_isend_irecv, interior overlapped)", 3
+        for s_, o in zip(slabs, outs):
+            s_.out = o[0]
+        dist.barrier()                 # every slab is complete before any neighbour reads it
 
         def step(i):
             slabs[i % pool].step()
-        launches_per_step = 3
         use_graph = False
     else:
         def step(i):
@@ -556,7 +568,7 @@ def run_ours(args):
                        "image": [h, w], "input": "uint8 pixels" if kind == "u8" else
                        "packed u32 row words", "parallelism":
                        {"batch": f"batch-shard x{world}" + ("" if weak_batch else " (strong)"),
-                        "rows": f"row-shard x{world} + NCCL halo",
+                        "rows": f"row-shard x{world}, halo: {halo_mode or 'none (1 rank)'}",
                         "replica": f"replicas x{world}"}[shard],
                        "l2_policy": f"rotating pool of {pool} input/output sets "
                                     f"({pool * step_bytes / 2**20:.0f} MiB > 3x L2 "
@@ -617,6 +629,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
+                    help="row-sharded configs: halo rows by peer reads in the kernel or NCCL")
     ap.add_argument("--strong", action="store_true",
                     help="batch configs: split one batch across ranks instead of one batch per rank")
     ap.add_argument("--streams", type=int, default=3,

@@ -165,6 +165,16 @@ int be_p4_encode(const void *in, uint8_t *p4, int word_bits, int64_t n, int64_t 
 int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int64_t h, int64_t w,
                 int fill_bit, uint32_t *scratch_or_null, void *stream);
 
+/* ---- peer-memory halos (multi-GPU row sharding without a separate exchange) --
+ * A rank exports its slab with be_ipc_export (64-byte cudaIpcMemHandle_t plus
+ * the pointer's offset inside its allocation); its row neighbours import it with
+ * be_ipc_open and pass pointers to the neighbour's boundary rows straight to
+ * be_edge_packed_halo_u32 as `above` / `below`: the halo rows are then read over
+ * NVLink by the edge kernel itself. */
+int be_ipc_export(const void *dev_ptr, void *handle_out, int64_t *offset_out);
+int be_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
+int be_ipc_close(void *dev_ptr, int64_t offset);
+
 /* ---- host buffers (the end-to-end path) ----------------------------------- */
 
 /* Edges of a batch that lives in HOST memory (pinned for overlap): uint8 pixels

@@ -49,6 +49,9 @@ _SIGNATURES = {
     "be_p4_decode": [_P, _P, _INT, _I64, _I64, _I64, _I64, _P],
     "be_p4_encode": [_P, _P, _INT, _I64, _I64, _I64, _I64, _P],
     "be_p4_edges": [_P, _P, _I64, _I64, _I64, _INT, _P, _P],
+    "be_ipc_export": [_P, _P, ctypes.POINTER(_I64)],
+    "be_ipc_open": [_P, _I64, ctypes.POINTER(_P)],
+    "be_ipc_close": [_P, _I64],
     "be_host_edges": [_P, _INT, _P, _I64, _I64, _I64, _INT, ctypes.POINTER(_P),
                       ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_last_error": [],

@@ -1031,6 +1031,49 @@ int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int6
                       stream, threshold);
 }
 
+// ---- peer-memory halos: CUDA IPC export / import of a device buffer --------
+
+typedef int (*cuMemGetAddressRange_t)(unsigned long long *, size_t *, unsigned long long);
+
+int be_ipc_export(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
+    if (dev_ptr == nullptr || handle_out == nullptr || offset_out == nullptr)
+        return fail(BE_EINVAL, "NULL argument");
+    // the IPC handle names the whole allocation: find its base through the driver
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr)
+        return fail(e != cudaSuccess ? (int)e : BE_EINVAL, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (((cuMemGetAddressRange_t)fn)(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return fail(BE_EINVAL, "pointer is not a device allocation");
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((uintptr_t)dev_ptr - base);
+    return BE_OK;
+}
+
+int be_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out) {
+    if (handle == nullptr || dev_ptr_out == nullptr) return fail(BE_EINVAL, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *dev_ptr_out = (char *)base + offset;
+    return BE_OK;
+}
+
+int be_ipc_close(void *dev_ptr, int64_t offset) {
+    if (dev_ptr == nullptr) return fail(BE_EINVAL, "NULL argument");
+    cudaError_t e = cudaIpcCloseMemHandle((char *)dev_ptr - offset);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return BE_OK;
+}
+
 int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
                   int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
                   int64_t chunk_images, void *stream0, void *stream1, int blocking) {

@@ -5,12 +5,13 @@ with no distributed code; this layer is new.
 * Batch sharding (configs C2, C5): rank r owns images [lo, hi) of the batch
   (`shard_range`); the images are independent, so there is no collective on
   the data path.
-* Row sharding (config C4): rank r owns rows [lo, hi) of one giant raster.
-  The only exchange is one packed row to each row neighbour (`exchange_halos`,
-  grouped NCCL send/recv over NVLink, 8 KiB per message at 65536 px).  The
-  interior rows, which need no halo, are computed while the exchange is in
-  flight; the two boundary rows follow with the received halos (kernel K3).
-  Ranks 0 and G-1 use the border fill on their outer side (bitimage.py:216-223).
+* Row sharding (config C4): rank r owns rows [lo, hi) of one giant raster;
+  ranks 0 and G-1 use the border fill on their outer side (bitimage.py:216-223).
+  `PeerHaloEdges`: the edge kernel reads the neighbours' boundary rows straight
+  from their HBM over NVLink (CUDA IPC peer pointers) -- one launch per step.
+  `RowShardedEdges`: one packed row to each row neighbour by grouped NCCL
+  send/recv (8 KiB per message at 65536 px) while the interior rows, which need
+  no halo, are computed; then the two boundary rows with the received halos.
 """
 
 from __future__ import annotations
@@ -118,3 +119,67 @@ class RowShardedEdges:
         if rows > 1:
             self.compute(self.slab, above, below, self.out, rows - 1, rows)
         return self.out
+
+
+class PeerHaloEdges:
+    """Row-sharded edges whose halo rows are read from the neighbour ranks'
+    slabs over NVLink by the edge kernel itself (CUDA IPC peer pointers passed
+    as K3's `above` / `below`): no exchange step and one launch per step -- the
+    fused alternative to `RowShardedEdges`' NCCL send/recv.
+
+    Setup exports this rank's slab (`be_ipc_export`), all-gathers the handles and
+    opens the row neighbours' (`be_ipc_open`).  Each step reads the neighbours'
+    boundary rows as they are in HBM at that moment, so the caller must make
+    every rank's slab complete before the step (a barrier after the producer;
+    the benchmark's slabs are written once before timing)."""
+
+    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None):
+        import ctypes
+
+        from . import _capi
+
+        self._capi, self._ct = _capi, ctypes
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if slab.dim() != 2 or slab.dtype != torch.int32 or not slab.is_cuda or \
+                slab.stride(1) != 1:
+            raise ValueError("slab must be a row-contiguous CUDA int32 [rows, S] tensor")
+        self.slab, self.width, self.border = slab, int(width), border
+        self.rows, self.stride = slab.shape[0], slab.stride(0)
+        self.out = torch.empty_like(slab)
+        handle = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _capi.call("be_ipc_export", ctypes.c_void_p(slab.data_ptr()), handle, ctypes.byref(off))
+        mine = (bytes(handle), off.value, self.rows, self.stride)
+        everyone = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []
+        self.above_ptr = self._open(everyone[self.rank - 1], last_row=True) if self.rank > 0 else None
+        self.below_ptr = (self._open(everyone[self.rank + 1], last_row=False)
+                          if self.rank < self.world - 1 else None)
+
+    def _open(self, info, last_row: bool) -> int:
+        ct = self._ct
+        handle, off, rows, stride = info
+        ptr = ct.c_void_p()
+        self._capi.call("be_ipc_open", ct.create_string_buffer(handle, 64), off, ct.byref(ptr))
+        self._opened.append((ptr.value, off))
+        return ptr.value + ((rows - 1) * stride * 4 if last_row else 0)
+
+    def step(self) -> torch.Tensor:
+        ct = self._ct
+        from . import cuda as cu
+
+        self._capi.call("be_edge_packed_halo_u32", ct.c_void_p(self.slab.data_ptr()),
+                        ct.c_void_p(self.above_ptr) if self.above_ptr else None,
+                        ct.c_void_p(self.below_ptr) if self.below_ptr else None,
+                        ct.c_void_p(self.out.data_ptr()), self.rows, self.width, self.stride,
+                        cu.fill_bit(self.border), 0, self.rows,
+                        ct.c_void_p(torch.cuda.current_stream().cuda_stream))
+        return self.out
+
+    def close(self):
+        for ptr, off in self._opened:
+            self._capi.call("be_ipc_close", self._ct.c_void_p(ptr), off)
+        self._opened = []

@@ -1,0 +1,62 @@
+"""Peer-memory halos (PeerHaloEdges): two ranks on ONE GPU exchange CUDA IPC
+handles over gloo and each runs a single edge kernel that reads its
+neighbour's boundary row straight from the other process's allocation.  No
+kernel waits on another (the slabs are written before a barrier), so sharing
+one device is safe; on an 8-GPU box the same pointers resolve over NVLink."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, H, W, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import cscan
+        from oracle import port as P
+        from paper_1401_5245_b200.dist import PeerHaloEdges, shard_range
+
+        rng = np.random.default_rng(123)
+        img = (rng.random((H, W)) < 0.5).astype(np.uint8)
+        packed = P.pack_u32(img)
+        lo, hi = shard_range(H, rank, world)
+        slab = torch.from_numpy(packed[lo:hi].view(np.int32).copy()).cuda()
+        torch.cuda.synchronize()
+        ph = PeerHaloEdges(slab, W, 1)
+        dist.barrier()                      # every slab is in HBM before anyone reads it
+        out = ph.step().cpu().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+        exp = cscan.scan_p32(packed, W, 1)[lo:hi]
+        ok = bool((out == exp).all())
+        dist.barrier()                      # neighbours done reading before memory goes away
+        ph.close()
+        res = [None] * world
+        dist.all_gather_object(res, ok)
+        if rank == 0:
+            q.put(all(res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_halo_two_processes_one_gpu(world, cuda_dev):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker, args=(world, _port(), 150, 8192, q), nprocs=world, join=True)
+    assert q.get(timeout=120) is True
