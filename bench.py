@@ -302,7 +302,7 @@ def run_ours(args):
     from paper_1401_5245_b200.host import HostBatchEdges
 
     rank, world = bd.init()
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = bd.env_rank_world()[2]
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = args.config
@@ -510,7 +510,7 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1:        # captured per launch at N = 1
         with open(tp) as f:
             traffic = json.load(f).get(cfg)
 
@@ -575,7 +575,9 @@ def run_ours(args):
                                     f"{l2 / 2**20:.0f} MiB)" if pool > 1 else
                                     f"step footprint {step_bytes / 2**20:.0f} MiB > L2",
                        "launch": ("CUDA graph replay" if use_graph else "direct launches")
-                                 + f", independent steps on {args.streams} parallel streams"},
+                                 + (f", independent steps on {args.streams} parallel streams"
+                                    if args.streams > 1 and not (shard == "rows" and world > 1)
+                                    else ", one stream")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,

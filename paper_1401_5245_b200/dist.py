@@ -32,8 +32,13 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def env_rank_world() -> tuple[int, int, int]:
-    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+    """(rank, world, device index).  BITEDGE_SHARE_GPU=1 maps every rank onto
+    device 0 -- a functional test of the multi-rank paths on a one-GPU box (the
+    timings of such a run mean nothing)."""
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("BITEDGE_SHARE_GPU"):
+        local = 0
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), local
 
 
 def init(backend: str | None = None) -> tuple[int, int]:
@@ -41,7 +46,8 @@ def init(backend: str | None = None) -> tuple[int, int]:
     rank, world, local = env_rank_world()
     if world > 1 and not dist.is_initialized():
         if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = os.environ.get("BITEDGE_DIST_BACKEND") or (
+                "nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group(backend, device_id=torch.device("cuda", local))
