@@ -899,7 +899,7 @@ int be_pack_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int6
                     int64_t in_row_stride, int64_t out_row_stride_words, int fill_bit,
                     uint32_t *packed_in_or_null, void *stream) {
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
     return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, packed_in_or_null,
                       32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream);
 }
@@ -917,7 +917,7 @@ int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
 int be_pack_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
                int64_t in_row_stride, int64_t out_row_stride_words, void *stream) {
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
     return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
                       (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
                       stream);
@@ -932,7 +932,7 @@ int be_unpack_u8(const void *in, uint8_t *out, int word_bits, int64_t n, int64_t
     if (out_row_stride < w) return fail(BE_EINVAL, "output row stride < width");
     if (n == 0) return BE_OK;
     if ((rc = check_ptr(in, word_bits, "input"))) return rc;
-    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
     WordGeom g = word_geom(G, in_row_stride_words);
     unpack_kernel<<<grid_for(g.nrows * (g.pl + 1)), 256, 0, S(stream)>>>(
         (const uint32_t *)in, out, g, w, out_row_stride);
@@ -1016,7 +1016,7 @@ int be_threshold_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h,
                          int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
                          int fill_bit, uint32_t *binary_or_null, void *stream) {
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
     return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, binary_or_null,
                       32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream, threshold);
 }
@@ -1025,7 +1025,7 @@ int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int6
                     int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
                     void *stream) {
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
     return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
                       (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
                       stream, threshold);

@@ -451,3 +451,24 @@ def test_pbm_roundtrip_and_detect(cuda_dev):
             out = detect_pbm(p4)
             payload = np.frombuffer(out[-((w + 7) // 8) * h:], np.uint8).reshape(h, -1)
             assert not (payload[:, -1] & ((1 << (8 - w % 8)) - 1)).any()
+
+
+# ---------------------------------------------------------------- extremes
+
+def test_empty_batch_and_extreme_shapes(cuda_dev):
+    """n = 0 is a no-op; one very long row, one very tall column and a wide
+    3-row strip agree with the oracle (grid-size and tail handling)."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    empty = torch.zeros((0, 5, 40), dtype=torch.uint8, device=cuda_dev)
+    assert cu.pack_edges_u8(empty).shape == (0, 5, 2)
+    assert cu.edges_packed(torch.zeros((0, 5, 2), dtype=torch.int32, device=cuda_dev), 40).shape[0] == 0
+    rng = np.random.default_rng(9)
+    for (n, h, w) in [(1, 1, 1 << 20), (1, 1 << 18, 1), (1, 3, 100003), (2, 1 << 12, 33)]:
+        a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
+        exp = cscan.scan_u8(a, 1)
+        assert (_u32(cu.pack_edges_u8(_t(a, cuda_dev), 1)) == exp).all(), (n, h, w)
+        pk = _t(P.pack_u32(a).view(np.int32), cuda_dev)
+        assert (_u32(cu.edges_packed(pk, w, 0)) == cscan.scan_u8(a, 0)).all(), (n, h, w)
