@@ -580,6 +580,7 @@ def run_ours(args):
                                     else ", one stream")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_of_nominal_8000": achieved / 8000.0,
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes,
                          "avg_launch_us": per_launch_ms * 1e3,
