@@ -530,10 +530,20 @@ def run_ours(args):
                 dist.barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # step i is enqueued before step i-1's result is awaited and read on the
+            # host (two host output buffers), so the CPU-side sync latency of one
+            # step hides behind the next step's copies
+            houts = [hout, torch.empty_like(hout, pin_memory=True)]
+            done = [torch.cuda.Event(), torch.cuda.Event()]
             e0.record()
-            for _ in range(e2e_steps):
-                pipe(hin, hout, sync=True)  # waits for this step's D2H
-                _ = int(hout[0, 0, 0])      # the step's result, read on the host
+            for i in range(e2e_steps):
+                pipe(hin, houts[i & 1], sync=False)
+                done[i & 1].record()
+                if i > 0:
+                    done[(i - 1) & 1].synchronize()
+                    _ = int(houts[(i - 1) & 1][0, 0, 0])   # step i-1's result, on the host
+            done[(e2e_steps - 1) & 1].synchronize()
+            _ = int(houts[(e2e_steps - 1) & 1][0, 0, 0])
             e1.record()
             torch.cuda.synchronize()
             ems = e0.elapsed_time(e1)
