@@ -97,3 +97,40 @@ def test_fuzz_p4(seed, cuda_dev):
         if w % 8:
             assert not (out[..., -1] & ((1 << (8 - w % 8)) - 1)).any()
         os.environ.pop("BITEDGE_P4_UNFUSED", None)
+
+
+@pytest.mark.parametrize("knob", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
+def test_fuzz_halo_slabs_all_inputs(knob, cuda_dev, monkeypatch):
+    """Row slabs with halo rows through be_edges_general for uint8 pixels, u32
+    words and u64 words: slab results concatenated == whole-image oracle."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    for k, v in knob.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(len(knob) * 7 + 1)
+    for (H, W) in [(41, 2048), (23, 100), (37, 4096), (9, 64)]:
+        a = (rng.random((H, W)) < 0.5).astype(np.uint8) * rng.integers(1, 256, (H, W)).astype(np.uint8)
+        exp = cscan.scan_u8(a, 1)
+        cuts = sorted({0, H, *rng.integers(1, H, 3).tolist()})
+        views = {
+            "u8": (torch.from_numpy(a).to(cuda_dev), 32),
+            "u32": (torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev), 32),
+            "u64": (torch.from_numpy(P.from_array(a).words.view(np.int64)).to(cuda_dev), 64),
+        }
+        for name, (full, wb) in views.items():
+            parts = []
+            for lo, hi in zip(cuts[:-1], cuts[1:]):
+                slab = full[lo:hi].clone()
+                above = full[lo - 1].clone() if lo > 0 else None
+                below = full[hi].clone() if hi < H else None
+                res = cu.edges_general(slab.unsqueeze(0), W, 1, word_bits=wb, above=above,
+                                       below=below)
+                parts.append(res["edges"][0])
+            got = torch.cat(parts).cpu().numpy()
+            if wb == 64:
+                got = P.u64_to_u32_rows(got.view(np.uint64))[:, : -(-W // 32)]
+            else:
+                got = got.view(np.uint32)
+            assert (got == exp).all(), (knob, name, H, W, cuts)
