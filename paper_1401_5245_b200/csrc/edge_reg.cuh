@@ -689,6 +689,7 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     const uint32_t seg_bytes = (uint32_t)(b_hi - b_lo);
     const int dst_off = (int)(b_lo - (x0 - 16));
     constexpr int NST = RSL + 2;
+    static_assert(RSL >= 2, "fetch order needs two own rows");
     // staged rows i in [i_lo, i_hi) lie inside `in`; row 0 / row lim may be halos
     const int i_lo = g0 == 0 ? 1 : 0;
     const int64_t lim = p.nrows - (g0 - 1);
@@ -699,17 +700,20 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     auto exists = [&](int i) {
         return (i >= i_lo && i < i_hi) || (top_halo && i == 0) || (bot_halo && i == i_hi);
     };
-    auto issue = [&](int i) {                        // lane 0 only
-        if (i >= NST || !exists(i)) return;
+    auto order = [&](int k) { return k == 0 ? NST - 1 : (k == NST - 1 ? 0 : k); };
+    auto issue = [&](int k) {                        // lane 0 only; k = fetch position
+        if (k >= NST) return;
+        const int i = order(k);
+        if (!exists(i)) return;
         const char *src = base + i * rb;
         if (top_halo && i == 0) src = p.above + b_lo;
         if (bot_halo && i == i_hi) src = p.below + b_lo;
-        uint64_t *b = &bars[i % D];
+        uint64_t *b = &bars[k % D];
         wbar_expect(b, seg_bytes);
-        wtma(ring + (i % D) * SLOT + dst_off, src, seg_bytes, b);
+        wtma(ring + (k % D) * SLOT + dst_off, src, seg_bytes, b);
     };
     if (lane == 0)
-        for (int i = 0; i < D; ++i) issue(i);
+        for (int k = 0; k < D; ++k) issue(k);
 
     auto tail_consts = [&](int c, uint32_t &keep, uint32_t &fixb, uint32_t &force) {
         keep = 0xFFFFFFFFu; fixb = 0u; force = 0u;
@@ -720,64 +724,87 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     tail_consts(ca, ka, fa, ga);
     tail_consts(cb, kb, fb, gb);
     const bool la = ca < p.wp, lb_ = cb < p.wp;
-    uint32_t y = (uint32_t)(g0 % p.h);
-    int64_t o = g0 * p.out_stride + ca;
+    const uint32_t y0 = (uint32_t)(g0 % p.h);
     uint32_t phase = 0u;
-    uint32_t ua = 0, ub = 0, xa = 0, xb = 0, el = 0, er = 0;   // up row, centre row, edge pixels
-    for (int i = 0; i < NST; ++i) {
-        const int slot = i % D;
-        uint32_t na = 0xFFFFFFFFu, nb = 0xFFFFFFFFu, nel = 0u, ner = 0u;
+    // One staged row: wait for its slot, pack both words, free the slot and
+    // refill it with the row D positions later in the fetch order.
+    auto fetch = [&](int k, uint32_t &a, uint32_t &b, uint32_t &el, uint32_t &er) {
+        const int i = order(k), slot = k % D;
+        a = 0xFFFFFFFFu; b = 0xFFFFFFFFu; el = 0u; er = 0u;
         if (exists(i)) {
             wbar_wait(&bars[slot], (phase >> slot) & 1u);
             phase ^= 1u << slot;
             const char *s = ring + slot * SLOT + 16;
-            na = pack32_any(*reinterpret_cast<const uint4 *>(s + 32 * lane),
-                            *reinterpret_cast<const uint4 *>(s + 32 * lane + 16), T);
-            nb = pack32_any(*reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane),
-                            *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16), T);
-            if (lane == 0) nel = (uint8_t)s[-1] >= T.t ? 1u : 0u;
-            if (lane == 31) ner = (uint8_t)s[SEG] >= T.t ? 0x80000000u : 0u;
+            a = pack32_any(*reinterpret_cast<const uint4 *>(s + 32 * lane),
+                           *reinterpret_cast<const uint4 *>(s + 32 * lane + 16), T);
+            b = pack32_any(*reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane),
+                           *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16), T);
+            if (lane == 0) el = (uint8_t)s[-1] >= T.t ? 1u : 0u;
+            if (lane == 31) er = (uint8_t)s[SEG] >= T.t ? 0x80000000u : 0u;
         }
         __syncwarp();
-        if (lane == 0) issue(i + D);                 // slot free (consumed or unused)
-        if (i >= 2) {
-            const int r = i - 2;                     // output row: up = ua/ub, centre = xa/xb, down = na/nb
-            const uint32_t a_up = __shfl_up_sync(0xFFFFFFFFu, xa, 1);
-            const uint32_t a_dn = __shfl_down_sync(0xFFFFFFFFu, xa, 1);
-            const uint32_t b_up = __shfl_up_sync(0xFFFFFFFFu, xb, 1);
-            const uint32_t b_dn = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
-            const uint32_t a31 = __shfl_sync(0xFFFFFFFFu, xa, 31);   // word 31 (left of word 32)
-            const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, xb, 0);     // word 32 (right of word 31)
-            const uint32_t lwa = lane == 0 ? (ca == 0 ? fw : el) : a_up;
-            const uint32_t rwa = lane == 31 ? b0 : a_dn;
-            const uint32_t lwb = lane == 0 ? a31 : b_up;
-            const uint32_t rwb = lane == 31 ? er : b_dn;
-            if (g0 + r < p.row_hi) {
-                const bool top = y == 0 && !(HALO && p.above);
-                const bool bot = y == p.h - 1 && !(HALO && p.below);
-                const uint32_t uA = top ? fw : ua, uB = top ? fw : ub;
-                const uint32_t dA = bot ? fw : na, dB = bot ? fw : nb;
-                const uint32_t lnA = __funnelshift_r(xa, lwa, 1);
-                const uint32_t rnA = (__funnelshift_l(rwa, xa, 1) & ka) | fa;
-                const uint32_t anyA = lnA | rnA | uA | dA;
-                const uint32_t lnB = __funnelshift_r(xb, lwb, 1);
-                const uint32_t rnB = (__funnelshift_l(rwb, xb, 1) & kb) | fb;
-                const uint32_t anyB = lnB | rnB | uB | dB;
-                if (la) {
-                    if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
-                    if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
-                }
-                if (lb_) {
-                    if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
-                    if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
-                }
+        if (lane == 0) issue(k + D);                 // slot free (consumed or unused)
+    };
+    // Output row r of the strip: up / centre / down words of both halves.
+    auto emit = [&](int r, uint32_t y, uint32_t ua, uint32_t ub, uint32_t xa, uint32_t xb,
+                    uint32_t na, uint32_t nb, uint32_t el, uint32_t er) {
+        const uint32_t a_up = __shfl_up_sync(0xFFFFFFFFu, xa, 1);
+        const uint32_t a_dn = __shfl_down_sync(0xFFFFFFFFu, xa, 1);
+        const uint32_t b_up = __shfl_up_sync(0xFFFFFFFFu, xb, 1);
+        const uint32_t b_dn = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
+        const uint32_t a31 = __shfl_sync(0xFFFFFFFFu, xa, 31);   // word 31 (left of word 32)
+        const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, xb, 0);     // word 32 (right of word 31)
+        const uint32_t lwa = lane == 0 ? (ca == 0 ? fw : el) : a_up;
+        const uint32_t rwa = lane == 31 ? b0 : a_dn;
+        const uint32_t lwb = lane == 0 ? a31 : b_up;
+        const uint32_t rwb = lane == 31 ? er : b_dn;
+        if (g0 + r < p.row_hi) {
+            const int64_t o = (g0 + r) * p.out_stride + ca;
+            const bool top = y == 0 && !(HALO && p.above);
+            const bool bot = y == p.h - 1 && !(HALO && p.below);
+            const uint32_t uA = top ? fw : ua, uB = top ? fw : ub;
+            const uint32_t dA = bot ? fw : na, dB = bot ? fw : nb;
+            const uint32_t lnA = __funnelshift_r(xa, lwa, 1);
+            const uint32_t rnA = (__funnelshift_l(rwa, xa, 1) & ka) | fa;
+            const uint32_t anyA = lnA | rnA | uA | dA;
+            const uint32_t lnB = __funnelshift_r(xb, lwb, 1);
+            const uint32_t rnB = (__funnelshift_l(rwb, xb, 1) & kb) | fb;
+            const uint32_t anyB = lnB | rnB | uB | dB;
+            if (la) {
+                if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
+                if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
             }
-            o += p.out_stride;
-            if (++y == p.h) y = 0;
+            if (lb_) {
+                if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
+                if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
+            }
         }
-        ua = xa; ub = xb; xa = na; xb = nb;
-        el = nel; er = ner;
+    };
+    // Fetch order: below-halo row first (it is the NEXT strip's first row, which
+    // that warp fetches at the same moment), then the strip's own rows, and the
+    // above-halo row last (the PREVIOUS strip's last row, fetched by that warp at
+    // the same moment).  The two shared rows are then read from DRAM once and
+    // served to the second reader from L2: ncu showed 2/RSL extra DRAM reads
+    // with the in-order fetch.
+    uint32_t dwa, dwb, t0, t1;                        // below halo (staged NST-1)
+    fetch(0, dwa, dwb, t0, t1);
+    uint32_t c0a, c0b, el0, er0;                      // staged 1 = output row 0's centre
+    fetch(1, c0a, c0b, el0, er0);
+    uint32_t ua = c0a, ub = c0b, xa, xb, el, er;      // staged 2
+    fetch(2, xa, xb, el, er);
+    const uint32_t c1a = xa, c1b = xb;
+    uint32_t y = y0 + 1 >= p.h ? (y0 + 1) % p.h : y0 + 1;
+    for (int k = 3; k < NST - 1; ++k) {               // output rows 1 .. RSL-2
+        uint32_t na, nb, nel, ner;
+        fetch(k, na, nb, nel, ner);
+        emit(k - 2, y, ua, ub, xa, xb, na, nb, el, er);
+        if (++y == p.h) y = 0;
+        ua = xa; ub = xb; xa = na; xb = nb; el = nel; er = ner;
     }
+    emit(RSL - 1, y, ua, ub, xa, xb, dwa, dwb, el, er);
+    uint32_t upa, upb;                                // above halo (staged 0)
+    fetch(NST - 1, upa, upb, t0, t1);
+    emit(0, y0, upa, upb, c0a, c0b, c1a, c1b, el0, er0);
 }
 
 }  // namespace bitedge

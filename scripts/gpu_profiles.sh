@@ -14,3 +14,8 @@ for c in ${CONFIGS:-c1 c2 c3 c4 c5}; do
   KB_NOGRAPH=6 ncu --set full --clock-control none --import-source on -k regex:edge_ -s 4 -c 1 \
       -o gpurun_out/prof/full_$c -f $CMD > gpurun_out/prof/ncu_full_$c.log 2>&1
 done
+# summarise on the box (ncu -i is here too) so only small files need to travel back
+PROF_DST=gpurun_out/prof/summary python scripts/summarize_profiles.py ${TAG:-r1} > /dev/null 2>&1
+ls -la gpurun_out/prof > gpurun_out/prof/ls.txt
+for r in gpurun_out/prof/full_c*.ncu-rep; do [ "$(stat -c %s $r)" -gt 12000000 ] && rm -f $r; done
+true

@@ -13,7 +13,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out", "prof")
-DST = os.path.join(ROOT, "profiles")
+DST = os.environ.get("PROF_DST", os.path.join(ROOT, "profiles"))
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
 ALG = {"c1": 256 * 256 * 1.125, "c2": 4096 * 64 * 64 * 1.125, "c3": 8192 * 8192 * 0.25,
        "c4": 65536 * 65536 * 0.25, "c5": 1024 * 2048 * 2048 * 1.125}
