@@ -570,7 +570,7 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     const uint32_t seg_bytes = (uint32_t)(b_hi - b_lo);
     const int dst_off = (int)(b_lo - (x0 - 16));     // 16 for the first segment, else 0
     const int nst = RSL + 2;                         // staged rows
-    const int64_t lim = p.nrows - (g0 - 1);          // staged rows i < lim exist (below: i == lim)
+    static_assert(RSL >= 2, "fetch order needs two own rows");
 
     // staged row i <-> global row g0-1+i; returns the row pointer or nullptr
     auto row_of = [&](int i) -> const char * {
@@ -582,16 +582,18 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
         }
         return nullptr;
     };
-    auto issue = [&](int i) {                        // lane 0 only
-        if (i >= nst) return;
-        const char *row = row_of(i);
+    // fetch order (see K2t2): below halo first, own rows, above halo last
+    auto order = [&](int k) { return k == 0 ? nst - 1 : (k == nst - 1 ? 0 : k); };
+    auto issue = [&](int k) {                        // lane 0 only; k = fetch position
+        if (k >= nst) return;
+        const char *row = row_of(order(k));
         if (row == nullptr) return;
-        uint64_t *b = &bars[i % D];
+        uint64_t *b = &bars[k % D];
         wbar_expect(b, seg_bytes);
-        wtma(ring + (i % D) * SLOT + dst_off, row + b_lo, seg_bytes, b);
+        wtma(ring + (k % D) * SLOT + dst_off, row + b_lo, seg_bytes, b);
     };
     if (lane == 0)
-        for (int i = 0; i < D; ++i) issue(i);
+        for (int k = 0; k < D; ++k) issue(k);
 
     uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
     if (c == p.pl) {
@@ -602,52 +604,61 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
         force = 0xFFFFFFFFu;
     }
     const bool live_col = c < p.wp;
-    uint32_t y = (uint32_t)(g0 % p.h);
-    int64_t o = g0 * p.out_stride + c;
+    const uint32_t y0 = (uint32_t)(g0 % p.h);
     uint32_t phase = 0u;                             // per-slot parity bits
-    uint32_t w_up = 0u, w_c = 0u, e_c = 0u;
-    for (int i = 0; i < nst; ++i) {
-        const int slot = i % D;
-        uint32_t w_new = 0xFFFFFFFFu, e_new = 0u;
-        if (row_of(i) != nullptr) {
+    auto fetch = [&](int k, uint32_t &w, uint32_t &e) {
+        const int slot = k % D;
+        w = 0xFFFFFFFFu; e = 0u;
+        if (row_of(order(k)) != nullptr) {
             wbar_wait(&bars[slot], (phase >> slot) & 1u);
             phase ^= 1u << slot;
             const char *src = ring + slot * SLOT + 16 + 32 * lane;
             const uint4 a = *reinterpret_cast<const uint4 *>(src);
             const uint4 b = *reinterpret_cast<const uint4 *>(src + 16);
-            w_new = pack32_any(a, b, T);
-            if (lane == 0) e_new = (uint8_t)src[-1] >= T.t ? 1u : 0u;
-            if (lane == 31) e_new = (uint8_t)src[32] >= T.t ? 0x80000000u : 0u;
+            w = pack32_any(a, b, T);
+            if (lane == 0) e = (uint8_t)src[-1] >= T.t ? 1u : 0u;
+            if (lane == 31) e = (uint8_t)src[32] >= T.t ? 0x80000000u : 0u;
         }
-        // slot i % D is free (consumed, or never filled because staged row i does
-        // not exist): refill it with staged row i + D
+        // the slot is free (consumed, or never filled because the row does not
+        // exist): refill it with the row D fetch positions later
         __syncwarp();
-        if (lane == 0) issue(i + D);
-        if (i >= 2) {
-            // output row r = i-2: up = staged i-2, centre = staged i-1, down = staged i
-            const int r = i - 2;
-            uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, w_c, 1);
-            uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, w_c, 1);
-            if (lane == 0) lw = e_c;
-            if (lane == 31) rw = e_c;
-            if (c == 0) lw = fw;
-            if (live_col && g0 + r < p.row_hi) {
-                const uint32_t u = (y == 0 && !(HALO && p.above)) ? fw : w_up;
-                const uint32_t d = (y == p.h - 1 && !(HALO && p.below)) ? fw : w_new;
-                const uint32_t ln = __funnelshift_r(w_c, lw, 1);
-                const uint32_t rn = (__funnelshift_l(rw, w_c, 1) & keep) | fixb;
-                const uint32_t any = ln | rn | u | d;
-                if (OUT != kOutEset) __stcs(p.o_edges + o, w_c | ~any | force);
-                if (OUT != kOutEdges) __stcs(p.o_eset + o, (~w_c & any) | force);
-            }
-            o += p.out_stride;
-            if (++y == p.h) y = 0;
+        if (lane == 0) issue(k + D);
+    };
+    auto emit = [&](int r, uint32_t y, uint32_t w_up, uint32_t w_c, uint32_t w_dn, uint32_t e_c) {
+        uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, w_c, 1);
+        uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, w_c, 1);
+        if (lane == 0) lw = e_c;
+        if (lane == 31) rw = e_c;
+        if (c == 0) lw = fw;
+        if (live_col && g0 + r < p.row_hi) {
+            const int64_t o = (g0 + r) * p.out_stride + c;
+            const uint32_t u = (y == 0 && !(HALO && p.above)) ? fw : w_up;
+            const uint32_t d = (y == p.h - 1 && !(HALO && p.below)) ? fw : w_dn;
+            const uint32_t ln = __funnelshift_r(w_c, lw, 1);
+            const uint32_t rn = (__funnelshift_l(rw, w_c, 1) & keep) | fixb;
+            const uint32_t any = ln | rn | u | d;
+            if (OUT != kOutEset) __stcs(p.o_edges + o, w_c | ~any | force);
+            if (OUT != kOutEdges) __stcs(p.o_eset + o, (~w_c & any) | force);
         }
-        w_up = w_c;
-        w_c = w_new;
-        e_c = e_new;
+    };
+    uint32_t w_dn_halo, w_c0, e_c0, w_c, e_c, t;
+    fetch(0, w_dn_halo, t);                          // staged nst-1 (below halo)
+    fetch(1, w_c0, e_c0);                            // staged 1: output row 0's centre
+    fetch(2, w_c, e_c);                              // staged 2
+    const uint32_t w_c1 = w_c;
+    uint32_t w_up = w_c0;
+    uint32_t y = y0 + 1 >= p.h ? (y0 + 1) % p.h : y0 + 1;
+    for (int k = 3; k < nst - 1; ++k) {              // output rows 1 .. RSL-2
+        uint32_t w_new, e_new;
+        fetch(k, w_new, e_new);
+        emit(k - 2, y, w_up, w_c, w_new, e_c);
+        if (++y == p.h) y = 0;
+        w_up = w_c; w_c = w_new; e_c = e_new;
     }
-    (void)lim;
+    emit(RSL - 1, y, w_up, w_c, w_dn_halo, e_c);
+    uint32_t w_up_halo;
+    fetch(nst - 1, w_up_halo, t);                    // staged 0 (above halo)
+    emit(0, y0, w_up_halo, w_c0, w_c1, e_c0);
 }
 
 // K2t2: same ring, but a warp owns a 2048-pixel row segment and every lane two
