@@ -108,5 +108,11 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args))
 
 
+def fn(name: str):
+    """The typed foreign function itself (hot callers check the rc only when
+    it is nonzero)."""
+    return getattr(_lib if _lib is not None else load(), name)
+
+
 def launch_count() -> int:
     return int(load().be_launch_count())

@@ -46,7 +46,14 @@ def _require_cuda(t: torch.Tensor, what: str) -> None:
         raise ValueError(f"{what} must be a CUDA tensor (there is no CPU path)")
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(t: torch.Tensor) -> int:
+    """The current stream of t's device as an integer handle (the ctypes
+    argtypes take ints; the raw getter skips torch.cuda.Stream's ~3 us)."""
+    if _raw_stream is not None:
+        return _raw_stream(t.get_device())
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
@@ -104,34 +111,97 @@ def _check_out(out: torch.Tensor, ref3: torch.Tensor, squeeze: bool, what="out")
 
 
 def _ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    return None if t is None else t.data_ptr()
 
 
 # ------------------------------------------------------------------ hot path
+
+def _dims(t: torch.Tensor, what: str):
+    """(n, h, s, row_stride) of a [H, S] / [N, H, S] tensor without building
+    views -- the same rules as _as3d + _row_stride, on the per-call hot path."""
+    d = t.dim()
+    if d == 2:
+        n = 1
+        h, s = t.shape
+        sh, ss = t.stride()
+        sn = 0
+    elif d == 3:
+        n, h, s = t.shape
+        sn, sh, ss = t.stride()
+    else:
+        raise ValueError(f"{what} must be [H, S] or [N, H, S], got shape {tuple(t.shape)}")
+    if s and ss != 1:
+        raise ValueError(f"{what}: rows must be contiguous")
+    rs = sh if h > 1 else max(s, sh)
+    if n > 1 and sn != h * rs:
+        raise ValueError(f"{what}: images of a batch must be contiguous")
+    return n, h, s, rs
+
 
 def edges_packed(words: torch.Tensor, width: int, border=WHITE_OUTSIDE, *, out=None,
                  edgeset: bool = False) -> torch.Tensor:
     """detect_edges_mask -- or the EdgeSet
     when `edgeset` -- of packed rasters, in one fused pass (kernel K1)."""
-    squeeze = words.dim() == 2
-    w3, wb, rs = _packed(words, width)
-    o = _new_like(w3, squeeze) if out is None else out
-    o3 = _check_out(o, w3, squeeze)
-    n, h, _ = w3.shape
-    ors = _row_stride(o3, "out")
+    _require_cuda(words, "words")
+    wb = word_bits_of(words)
+    n, h, s, rs = _dims(words, "words")
+    width = int(width)
+    if s < -(-width // wb):
+        raise ValueError(f"words: width {width} needs {words_per_row(width, wb)} words per row, "
+                         f"got {s}")
+    fb = fill_bit(border)
+    if out is None:
+        o = torch.empty(words.shape, dtype=words.dtype, device=words.device)
+        ors = s
+    else:
+        o = out
+        o3 = _check_out(o, _as3d(words, "words"), words.dim() == 2)
+        ors = _row_stride(o3, "out")
     if ors != rs:   # different input / output strides: the general entry point
         outs = _capi.be_outputs()
         if edgeset:
-            outs.edgeset = o3.data_ptr()
+            outs.edgeset = o.data_ptr()
         else:
-            outs.edges = o3.data_ptr()
-        _capi.call("be_edges_general", _ptr(w3), 0, rs, None, None, ctypes.byref(outs), wb, ors,
-                   n, h, int(width), fill_bit(border), 0, n * h, ctypes.c_void_p(_stream(w3)))
+            outs.edges = o.data_ptr()
+        _capi.call("be_edges_general", words.data_ptr(), 0, rs, None, None, ctypes.byref(outs), wb,
+                   ors, n, h, width, fb, 0, n * h, _stream(words))
         return o
-    name = "be_edge_packed_u64" if wb == 64 else "be_edge_packed_u32"
-    _capi.call(name, _ptr(w3), _ptr(o3), n, h, int(width), rs, fill_bit(border), int(edgeset),
-               ctypes.c_void_p(_stream(w3)))
+    rc = (_capi.fn("be_edge_packed_u64") if wb == 64 else _capi.fn("be_edge_packed_u32"))(
+        words.data_ptr(), o.data_ptr(), n, h, width, rs, fb, int(edgeset), _stream(words))
+    if rc:
+        _capi.check(rc)
     return o
+
+
+def pack_and_edges(pixels: torch.Tensor, border=WHITE_OUTSIDE, *, word_bits: int = 64,
+                   edgeset: bool = False):
+    """from_array + detect_edges_mask (or edge_set when `edgeset`) in ONE launch
+    that also writes the packed input: returns (edges, packed) in `word_bits`
+    words.  The drop-in BitImage uses it to fuse a deferred pack into edge
+    detection."""
+    _require_cuda(pixels, "pixels")
+    if pixels.dtype not in _PIXEL_DTYPES:
+        raise ValueError(f"pixels must be uint8/int8/bool (nonzero = white), got {pixels.dtype}")
+    n, h, w, prs = _dims(pixels, "pixels")
+    if w < 1 or h < 1:
+        raise ValueError(f"image dimensions must be at least 1x1, got {w}x{h}")
+    wp = -(-w // word_bits)
+    dt = torch.int64 if word_bits == 64 else torch.int32
+    shape = (n, h, wp) if pixels.dim() == 3 else (h, wp)
+    e = torch.empty(shape, dtype=dt, device=pixels.device)
+    pk = torch.empty(shape, dtype=dt, device=pixels.device)
+    o = _capi.be_outputs()
+    if edgeset:
+        o.edgeset = e.data_ptr()
+    else:
+        o.edges = e.data_ptr()
+    o.packed = pk.data_ptr()
+    rc = _capi.fn("be_edges_general")(pixels.data_ptr(), 1, prs, None, None, ctypes.byref(o),
+                                      word_bits, wp, n, h, w, fill_bit(border), 0, n * h,
+                                      _stream(pixels))
+    if rc:
+        _capi.check(rc)
+    return e, pk
 
 
 def _pixels(pixels: torch.Tensor, what="pixels"):
@@ -165,7 +235,7 @@ def pack_edges_u8(pixels: torch.Tensor, border=WHITE_OUTSIDE, *, out=None,
         if tuple(pk.shape) != shape or word_bits_of(pk) != 32 or _row_stride(pk, "packed_out") != ors:
             raise ValueError("packed_out must match out")
     _capi.call("be_pack_edge_u8", _ptr(p3), _ptr(o3), n, h, w, prs, ors, fill_bit(border), _ptr(pk),
-               ctypes.c_void_p(_stream(p3)))
+               _stream(p3))
     return o[0] if (squeeze and out is None) else o
 
 
@@ -194,7 +264,7 @@ def threshold_edges_u8(gray: torch.Tensor, threshold: int, border=WHITE_OUTSIDE,
         if tuple(bo.shape) != shape or word_bits_of(bo) != 32 or _row_stride(bo, "binary_out") != ors:
             raise ValueError("binary_out must match out")
     _capi.call("be_threshold_edge_u8", _ptr(p3), _ptr(o3), n, h, w, prs, ors, t, fill_bit(border),
-               _ptr(bo), ctypes.c_void_p(_stream(p3)))
+               _ptr(bo), _stream(p3))
     return o[0] if (squeeze and out is None) else o
 
 
@@ -209,7 +279,7 @@ def threshold_u8(gray: torch.Tensor, threshold: int, word_bits: int = 32) -> tor
     shape = (n, h, words_per_row(w, word_bits))
     o = torch.empty(shape, dtype=torch.int64 if word_bits == 64 else torch.int32, device=p3.device)
     _capi.call("be_threshold_u8", _ptr(p3), _ptr(o), word_bits, n, h, w, prs,
-               _row_stride(o, "out"), t, ctypes.c_void_p(_stream(p3)))
+               _row_stride(o, "out"), t, _stream(p3))
     return o[0] if squeeze else o
 
 
@@ -268,7 +338,7 @@ def edges_general(inp: torch.Tensor, width: int | None = None, border=WHITE_OUTS
         row_hi = n * h
     _capi.call("be_edges_general", _ptr(src), kind, irs, _ptr(above), _ptr(below),
                ctypes.byref(o), wb, ors, n, h, int(width), fill_bit(border), int(row_lo),
-               int(row_hi), ctypes.c_void_p(_stream(src)))
+               int(row_hi), _stream(src))
     return res
 
 
@@ -294,7 +364,7 @@ def edges_halo(slab: torch.Tensor, above, below, width: int, border=WHITE_OUTSID
         row_hi = rows
     _capi.call("be_edge_packed_halo_u32", _ptr(slab), _ptr(above), _ptr(below), _ptr(o), rows,
                int(width), rs, fill_bit(border), int(row_lo), int(row_hi),
-               ctypes.c_void_p(_stream(slab)))
+               _stream(slab))
     return o
 
 
@@ -302,18 +372,29 @@ def edges_halo(slab: torch.Tensor, above, below, width: int, border=WHITE_OUTSID
 
 def pack_u8(pixels: torch.Tensor, word_bits: int = 32, out=None) -> torch.Tensor:
     """BitImage.from_array (bitimage.py:122-136) on the device."""
-    squeeze = pixels.dim() == 2
-    p3, prs = _pixels(pixels)
-    n, h, w = p3.shape
-    shape = (n, h, words_per_row(w, word_bits))
+    _require_cuda(pixels, "pixels")
+    if pixels.dtype not in _PIXEL_DTYPES:
+        raise ValueError(f"pixels must be uint8/int8/bool (nonzero = white), got {pixels.dtype}")
+    n, h, w, prs = _dims(pixels, "pixels")
+    if w < 1 or h < 1:
+        raise ValueError(f"image dimensions must be at least 1x1, got {w}x{h}")
+    wp = -(-w // word_bits)
     dt = torch.int64 if word_bits == 64 else torch.int32
-    o = out if out is not None else torch.empty(shape, dtype=dt, device=p3.device)
-    o3 = _as3d(o, "out")
-    if tuple(o3.shape) != shape or word_bits_of(o3) != word_bits:
-        raise ValueError(f"out must be {word_bits}-bit words of shape {shape}")
-    _capi.call("be_pack_u8", _ptr(p3), _ptr(o3), word_bits, n, h, w, prs, _row_stride(o3, "out"),
-               ctypes.c_void_p(_stream(p3)))
-    return o[0] if (squeeze and out is None) else o
+    if out is None:
+        shape = (n, h, wp) if pixels.dim() == 3 else (h, wp)
+        o = torch.empty(shape, dtype=dt, device=pixels.device)
+        ors = wp
+    else:
+        o = out
+        o3 = _as3d(o, "out")
+        if tuple(o3.shape) != (n, h, wp) or word_bits_of(o3) != word_bits:
+            raise ValueError(f"out must be {word_bits}-bit words of shape {(n, h, wp)}")
+        ors = _row_stride(o3, "out")
+    rc = _capi.fn("be_pack_u8")(pixels.data_ptr(), o.data_ptr(), word_bits, n, h, w, prs, ors,
+                                _stream(pixels))
+    if rc:
+        _capi.check(rc)
+    return o
 
 
 def unpack_u8(words: torch.Tensor, width: int, out=None) -> torch.Tensor:
@@ -327,7 +408,7 @@ def unpack_u8(words: torch.Tensor, width: int, out=None) -> torch.Tensor:
     if tuple(o3.shape) != (n, h, int(width)) or o3.dtype != torch.uint8:
         raise ValueError("out must be uint8 [N, H, W]")
     _capi.call("be_unpack_u8", _ptr(w3), _ptr(o3), wb, n, h, int(width), rs,
-               _row_stride(o3, "out"), ctypes.c_void_p(_stream(w3)))
+               _row_stride(o3, "out"), _stream(w3))
     return o[0] if (squeeze and out is None) else o
 
 
@@ -343,7 +424,7 @@ def _binary(name, op, a, b, width):
     o3 = _as3d(o, "out")
     n, h, _ = a3.shape
     _capi.call("be_bitop", op, _ptr(a3), _ptr(b3), _ptr(o3), wb, n, h,
-               int(width), rs, ctypes.c_void_p(_stream(a3)))
+               int(width), rs, _stream(a3))
     return o
 
 
@@ -366,7 +447,7 @@ def shift(words, width, direction: int, border=WHITE_OUTSIDE):
     o = _new_like(w3, squeeze)
     n, h, _ = w3.shape
     _capi.call("be_shift", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs, int(direction),
-               fill_bit(border), ctypes.c_void_p(_stream(w3)))
+               fill_bit(border), _stream(w3))
     return o
 
 
@@ -380,7 +461,7 @@ def shift_and(img, mask, width, side: int, border=WHITE_OUTSIDE):
     o = _new_like(i3, squeeze)
     n, h, _ = i3.shape
     _capi.call("be_shift_and", _ptr(i3), _ptr(m3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
-               int(side), fill_bit(border), ctypes.c_void_p(_stream(i3)))
+               int(side), fill_bit(border), _stream(i3))
     return o
 
 
@@ -390,7 +471,7 @@ def count_black(words, width) -> torch.Tensor:
     n, h, _ = w3.shape
     counts = torch.empty(n, dtype=torch.int64, device=w3.device)
     _capi.call("be_count_black", _ptr(w3), _ptr(counts), wb, n, h, int(width), rs,
-               ctypes.c_void_p(_stream(w3)))
+               _stream(w3))
     return counts
 
 
@@ -401,5 +482,5 @@ def scan_edges(words, width, border=WHITE_OUTSIDE):
     o = _new_like(w3, squeeze)
     n, h, _ = w3.shape
     _capi.call("be_scan_edges", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
-               fill_bit(border), ctypes.c_void_p(_stream(w3)))
+               fill_bit(border), _stream(w3))
     return o

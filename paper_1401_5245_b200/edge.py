@@ -54,18 +54,28 @@ def fundamental_edge(img: BitImage, mask: BitImage, side: Direction,
                                             side.code, border.fill_bit))
 
 
+def _edges(img: BitImage, border: BorderPolicy, edgeset: bool) -> BitImage:
+    pix = img._take_pixels()
+    if pix is not None:
+        # image from from_array, not packed yet: pack + edges in one launch
+        out, packed = _cuda().pack_and_edges(pix, border.fill_bit, edgeset=edgeset)
+        img._adopt_packed(packed)
+    else:
+        out = _cuda().edges_packed(img.device_words(), img.width, border.fill_bit,
+                                   edgeset=edgeset)
+    return BitImage._wrap(img.width, img.height, out)
+
+
 def detect_edges_mask(img: BitImage, border: BorderPolicy = _WHITE) -> BitImage:
     """invert(OR of the four fundamental EdgeSets): edge pixels black (0), all
-    others white (1), padding 1.  One kernel launch."""
-    return BitImage._wrap(img.width, img.height,
-                          _cuda().edges_packed(img.device_words(), img.width, border.fill_bit))
+    others white (1), padding 1.  One kernel launch -- which
+    also packs the image when it came from `from_array` and was not packed yet."""
+    return _edges(img, border, False)
 
 
 def edge_set(img: BitImage, border: BorderPolicy = _WHITE) -> BitImage:
     """The pre-inversion marker raster: 1 = edge pixel."""
-    return BitImage._wrap(img.width, img.height,
-                          _cuda().edges_packed(img.device_words(), img.width, border.fill_bit,
-                                               edgeset=True))
+    return _edges(img, border, True)
 
 
 def fundamental_edges(img: BitImage, border: BorderPolicy = _WHITE) -> dict:
