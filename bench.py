@@ -526,24 +526,27 @@ def run_ours(args):
             e2e_steps = max(3, min(steps, int(max(1, 2e9 / max(1, pipe.h2d_bytes)))))
             for _ in range(2):
                 pipe(hin, hout)
+            for _ in range(4):                   # warm the pipelined (submit) path too
+                pipe.submit(hin, hout)
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            # step i is enqueued before step i-1's result is awaited and read on the
-            # host (two host output buffers), so the CPU-side sync latency of one
-            # step hides behind the next step's copies
+            # step i is submitted before step i-1's result is awaited and read on
+            # the host (two host output buffers), so the CPU-side sync latency of
+            # one step and its last chunk's kernel + D2H hide behind the next
+            # step's H2D (HostBatchEdges.submit does not chain batches)
             houts = [hout, torch.empty_like(hout, pin_memory=True)]
-            done = [torch.cuda.Event(), torch.cuda.Event()]
+            pend = [None, None]
             e0.record()
+            e0.synchronize()                     # every submitted copy starts after e0
             for i in range(e2e_steps):
-                pipe(hin, houts[i & 1], sync=False)
-                done[i & 1].record()
+                pend[i & 1] = pipe.submit(hin, houts[i & 1])
                 if i > 0:
-                    done[(i - 1) & 1].synchronize()
-                    _ = int(houts[(i - 1) & 1][0, 0, 0])   # step i-1's result, on the host
-            done[(e2e_steps - 1) & 1].synchronize()
-            _ = int(houts[(e2e_steps - 1) & 1][0, 0, 0])
+                    res = pend[(i - 1) & 1].synchronize()
+                    _ = int(res[0, 0, 0])        # step i-1's result, on the host
+            res = pend[(e2e_steps - 1) & 1].synchronize()
+            _ = int(res[0, 0, 0])
             e1.record()
             torch.cuda.synchronize()
             ems = e0.elapsed_time(e1)

@@ -60,10 +60,7 @@ class HostBatchEdges:
         hout = torch.empty(self.out_shape, dtype=torch.int32, pin_memory=True)
         return hin, hout
 
-    def __call__(self, host_in: torch.Tensor, host_out: torch.Tensor | None = None,
-                 sync: bool = True) -> torch.Tensor:
-        """Run the batch; with sync=False the caller's current stream is made to
-        wait for the result and the host buffers must stay untouched until then."""
+    def _check(self, host_in, host_out):
         if tuple(host_in.shape) != self.in_shape or host_in.dtype != self.in_dtype:
             raise ValueError(f"host input must be {self.in_dtype} {self.in_shape}")
         if host_in.is_cuda or not host_in.is_contiguous():
@@ -72,15 +69,67 @@ class HostBatchEdges:
             host_out = torch.empty(self.out_shape, dtype=torch.int32, pin_memory=True)
         if host_out.is_cuda or not host_out.is_contiguous() or tuple(host_out.shape) != self.out_shape:
             raise ValueError(f"host output must be a contiguous CPU int32 tensor {self.out_shape}")
-        cur = torch.cuda.current_stream(self.device)
-        for s_ in self.streams:
-            s_.wait_stream(cur)
+        return host_out
+
+    def _run(self, host_in, host_out, blocking: bool) -> None:
         P = ctypes.c_void_p
         _capi.call("be_host_edges", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                    P(host_out.data_ptr()), self.n, self.h, self.width, cu.fill_bit(self.border),
                    self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
-                   P(self.streams[1].cuda_stream), 1 if sync else 0)
+                   P(self.streams[1].cuda_stream), 1 if blocking else 0)
+
+    def __call__(self, host_in: torch.Tensor, host_out: torch.Tensor | None = None,
+                 sync: bool = True) -> torch.Tensor:
+        """Run the batch, ordered after the caller's current stream; with
+        sync=False the current stream is made to wait for the result and the
+        host buffers must stay untouched until then."""
+        host_out = self._check(host_in, host_out)
+        cur = torch.cuda.current_stream(self.device)
+        for s_ in self.streams:
+            s_.wait_stream(cur)
+        self._run(host_in, host_out, sync)
         if not sync:
             for s_ in self.streams:
                 cur.wait_stream(s_)
         return host_out
+
+    def submit(self, host_in: torch.Tensor, host_out: torch.Tensor | None = None) -> "Pending":
+        """Enqueue the batch and return at once; the returned handle's
+        `synchronize()` yields `host_out` when its last chunk has landed.
+
+        Unlike `__call__(sync=False)` this does not tie the caller's stream to
+        the batch, so consecutive submits pipeline across batches: the next
+        batch's first host->device copy starts as soon as the copy engine is
+        free instead of after this batch's last kernel and device->host copy.
+        `host_in` must be ready on the host; both buffers must stay untouched
+        until `synchronize()` returns."""
+        host_out = self._check(host_in, host_out)
+        self._run(host_in, host_out, False)
+        evs = []
+        for s_ in self.streams:
+            e = torch.cuda.Event()
+            e.record(s_)
+            evs.append(e)
+        return Pending(evs, host_out)
+
+
+class Pending:
+    """A submitted host batch (`HostBatchEdges.submit`)."""
+
+    def __init__(self, events, host_out):
+        self._events = events
+        self.host_out = host_out
+
+    def query(self) -> bool:
+        return all(e.query() for e in self._events)
+
+    def synchronize(self) -> torch.Tensor:
+        for e in self._events:
+            e.synchronize()
+        return self.host_out
+
+    def wait(self, stream=None) -> None:
+        """Make `stream` (default: the current one) wait for the batch."""
+        stream = stream if stream is not None else torch.cuda.current_stream()
+        for e in self._events:
+            stream.wait_event(e)

@@ -362,6 +362,32 @@ def test_host_pipeline_e2e(cuda_dev):
     assert (out2.numpy().view(np.uint32)[0] == cscan.scan_p32(c3, 8192)).all()
 
 
+def test_host_pipeline_submit(cuda_dev):
+    """HostBatchEdges.submit: several batches in flight over two host output
+    buffers (the bench's e2e loop), each result exact when its handle syncs."""
+    import torch
+
+    from paper_1401_5245_b200 import synth
+    from paper_1401_5245_b200.host import HostBatchEdges
+
+    batches = [synth.c2_images(300, start=300 * k) for k in range(3)]   # distinct images
+    pipe = HostBatchEdges(tuple(batches[0].shape), kind="u8", chunk_images=64)
+    hins = [torch.empty(tuple(b.shape), dtype=torch.uint8, pin_memory=True) for b in batches]
+    for h_, b in zip(hins, batches):
+        h_.copy_(b)
+    houts = [torch.empty(pipe.out_shape, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    pend = [None, None]
+    for i in range(9):
+        pend[i & 1] = pipe.submit(hins[i % 3], houts[i & 1])
+        if i > 0:
+            j = i - 1
+            got = pend[j & 1].synchronize().numpy().view(np.uint32)
+            assert (got == cscan.scan_u8(batches[j % 3].numpy(), 1)).all(), j
+    got = pend[8 & 1].synchronize().numpy().view(np.uint32)
+    assert (got == cscan.scan_u8(batches[8 % 3].numpy(), 1)).all()
+    assert pend[0].query() and pend[1].query()
+
+
 def test_fill_policies_on_border_touching_figure(cuda_dev):
     """Interior invariance: pixels >= 2 from the border do not depend
     on the policy; border pixels do."""
