@@ -682,34 +682,46 @@ __global__ void unpack_kernel(const uint32_t *__restrict__ in, uint8_t *__restri
     }
 }
 
-// detect_edges_scan: per-pixel Edge(p), one bit at a time.
-__device__ __forceinline__ uint32_t pixel_at(const uint32_t *__restrict__ in, const WordGeom &g,
-                                             int64_t img_row0, int64_t x, int64_t y, int64_t w) {
-    if (x < 0 || y < 0 || x >= w || y >= g.h) return g.fillword & 1u;
-    const int64_t row = img_row0 + y;
-    const int pw = (int)(x >> 5);
-    return (in[row * g.stride + (pw ^ g.swap)] >> (31 - (x & 31))) & 1u;
+// detect_edges_scan: the paper's "traditional scanning",
+// Edge(p) = p' AND (n2 OR n4 OR n6 OR n8) evaluated pixel by pixel -- an
+// algorithm independent of the mask kernels (no word-wide shifts or ORs), used
+// as the full-size GPU cross-check.  A thread owns one
+// 32-pixel word: it loads the five words its pixels' neighbours can live in
+// (centre, above, below, left, right; the border fill where they fall outside)
+// once, then walks its 32 pixels one at a time.
+__device__ __forceinline__ uint32_t scan_word_at(const uint32_t *__restrict__ in, const WordGeom &g,
+                                                 int64_t row, int pw) {
+    return in[row * g.stride + (pw ^ g.swap)];
 }
 
 __global__ void scan_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, WordGeom g,
                             int64_t w) {
     const int64_t total = g.nrows * g.wp;
+    const uint32_t fill = g.fillword & 1u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = t / g.wp;
         const int pw = (int)(t - row * g.wp);
-        const int64_t y = row % g.h, r0 = row - y;
+        const int64_t y = row % g.h;
+        const uint32_t c = scan_word_at(in, g, row, pw);
+        const uint32_t up = y > 0 ? scan_word_at(in, g, row - 1, pw) : 0u;
+        const uint32_t dn = y + 1 < g.h ? scan_word_at(in, g, row + 1, pw) : 0u;
+        const uint32_t lw = pw > 0 ? scan_word_at(in, g, row, pw - 1) : 0u;
+        const uint32_t rw = pw + 1 < g.wp ? scan_word_at(in, g, row, pw + 1) : 0u;
         uint32_t word = 0;
         for (int b = 0; b < 32; ++b) {
             const int64_t x = (int64_t)pw * 32 + b;
             uint32_t bit = 1u;
             if (x < w) {
-                const uint32_t p = pixel_at(in, g, r0, x, y, w);
-                const uint32_t nb = pixel_at(in, g, r0, x, y - 1, w) |      // Fig. 1 n2
-                                    pixel_at(in, g, r0, x - 1, y, w) |      // n4
-                                    pixel_at(in, g, r0, x, y + 1, w) |      // n6
-                                    pixel_at(in, g, r0, x + 1, y, w);       // n8
-                bit = !(!p && nb);
+                const uint32_t p = (c >> (31 - b)) & 1u;
+                // n2 (above) and n6 (below): same column, rows y-1 / y+1
+                const uint32_t n2 = y > 0 ? (up >> (31 - b)) & 1u : fill;
+                const uint32_t n6 = y + 1 < g.h ? (dn >> (31 - b)) & 1u : fill;
+                // n4 (left): pixel x-1, in the previous word when b == 0
+                const uint32_t n4 = x == 0 ? fill : (b == 0 ? lw & 1u : (c >> (32 - b)) & 1u);
+                // n8 (right): pixel x+1, in the next word when b == 31
+                const uint32_t n8 = x + 1 >= w ? fill : (b == 31 ? rw >> 31 : (c >> (30 - b)) & 1u);
+                bit = !(!p && (n2 | n4 | n6 | n8));
             }
             word = (word << 1) | bit;
         }
@@ -834,14 +846,23 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
         const int cw = v8 ? 8 : 4;
         rp.items = (G.wp + cw - 1) / cw;
         rp.vst = 1;
-        rp.nstrips = (n * h + 3) / 4;
+        // 2-row strips for small rasters (twice the threads in flight), as try_reg does
+        const bool big = ((n * h + 3) / 4) * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
+        const int rs = big ? 4 : 2;
+        rp.nstrips = (n * h + rs - 1) / rs;
         const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
         if (grid <= 0x7FFFFFFFLL) {
-            if (cw == 8)
+            if (cw == 8 && rs == 4)
                 launch_k(edge_reg_packed_kernel<0, 4, 8, kOutEdges, false, true>, (unsigned)grid, 0,
                          st, rp);
-            else
+            else if (cw == 8)
+                launch_k(edge_reg_packed_kernel<0, 2, 8, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            else if (rs == 4)
                 launch_k(edge_reg_packed_kernel<0, 4, 4, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            else
+                launch_k(edge_reg_packed_kernel<0, 2, 4, kOutEdges, false, true>, (unsigned)grid, 0,
                          st, rp);
             return cuda_check("edge_reg_packed_kernel<P4>");
         }

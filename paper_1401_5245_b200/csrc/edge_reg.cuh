@@ -92,12 +92,17 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
 
 // Item = CW pixel words of one row (memory order == pixel order for uint32 rows;
 // uint64 rows swap the halves of each word pair).  RS rows per strip.
-// PBM P4 rows (1 = black, MSB-first bytes) <-> pixel-order words (1 = white):
-// byte-swap the little-endian load and invert.
-__device__ __forceinline__ uint32_t p4_word(uint32_t v) { return ~__byte_perm(v, 0, 0x0123); }
+// PBM P4 rows (1 = black, MSB-first bytes).  A little-endian
+// load of 4 P4 bytes is the pixel-order word with its bytes reversed (pi) and
+// inverted.  AND / OR / NOT commute with pi, so only the horizontal shifts need
+// pixel order: the P4 kernel keeps up / centre / down rows as loaded, byte-swaps
+// the centre row once for the funnel shifts (black polarity: ~Ln, ~Rn), swaps
+// the shifted result back, and evaluates the edge formula in the P4 domain:
+//   out = c & ~(pi(~Ln & ~Rn) & u & d)      (1 = black edge pixel)
+__device__ __forceinline__ uint32_t p4_pi(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
 template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 1)   // P4: 3 (4-row) or 4 CTAs/SM
 edge_reg_packed_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
@@ -128,23 +133,19 @@ edge_reg_packed_kernel(const RegParams p) {
             if (i == lim && p.below) { ptr = p.below + 4 * pw0; ok = live; }
         }
         if (ok) {
-            load_chunk<CW>(ptr, v[i]);
-            if (P4) {
-#pragma unroll
-                for (int q = 0; q < CW; ++q) v[i][q] = p4_word(v[i][q]);
-            }
+            load_chunk<CW>(ptr, v[i]);               // P4: raw bytes, converted per use
         } else {
 #pragma unroll
-            for (int q = 0; q < CW; ++q) v[i][q] = fw;
+            for (int q = 0; q < CW; ++q) v[i][q] = P4 ? ~fw : fw;
         }
         if (i >= 1 && i <= RS) {
             lwx[i - 1] = fw;
             rwx[i - 1] = 0u;
             if (ok && need_l) lwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? -2 : -1));
             if (ok && need_r) rwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? CW + 1 : CW));
-            if (P4) {
-                if (ok && need_l) lwx[i - 1] = p4_word(lwx[i - 1]);
-                if (ok && need_r) rwx[i - 1] = p4_word(rwx[i - 1]);
+            if (P4) {                                // pixel order, black polarity
+                lwx[i - 1] = (ok && need_l) ? p4_pi(lwx[i - 1]) : ~fw;
+                rwx[i - 1] = (ok && need_r) ? p4_pi(rwx[i - 1]) : 0xFFFFFFFFu;
             }
         }
     }
@@ -160,14 +161,14 @@ edge_reg_packed_kernel(const RegParams p) {
 #pragma unroll
         for (int q = 0; q < CW; ++q) {
             cu[q] = v[r][q ^ SWAP];
-            cc[q] = v[r + 1][q ^ SWAP];
+            cc[q] = P4 ? p4_pi(v[r + 1][q]) : v[r + 1][q ^ SWAP];   // P4: pixel order, 1 = black
             cd[q] = v[r + 2][q ^ SWAP];
         }
         uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cc[CW - 1], 1);
         uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
         if (lane == 0) lw = lwx[r];
         if (lane == 31) rw = rwx[r];
-        if (c == 0) lw = fw;
+        if (c == 0) lw = P4 ? ~fw : fw;
         const int64_t g = g0 + r;
         if (live && g < p.row_hi) {
             const bool top = (y == 0) && !(HALO && p.above);
@@ -180,12 +181,25 @@ edge_reg_packed_kernel(const RegParams p) {
                 const uint32_t ln = __funnelshift_r(cc[q], left, 1);
                 uint32_t rn = __funnelshift_l(right, cc[q], 1);
                 uint32_t f = 0u;
-                if (tail) fix_tail(pw0 + q, p, rn, f);
-                const uint32_t u = top ? fw : cu[q];
-                const uint32_t d = bot ? fw : cd[q];
-                const uint32_t a = ln | rn | u | d;
-                ve[q ^ SWAP] = P4 ? p4_word(cc[q] | ~a | f) : (cc[q] | ~a | f);
-                vs[q ^ SWAP] = (~cc[q] & a) | f;
+                if (P4) {
+                    // ln / rn are ~Ln / ~Rn here (black polarity)
+                    if (tail) {
+                        uint32_t rw_ = ~rn;
+                        fix_tail(pw0 + q, p, rw_, f);
+                        rn = ~rw_;
+                    }
+                    const uint32_t u = top ? ~fw : cu[q];
+                    const uint32_t d = bot ? ~fw : cd[q];
+                    ve[q] = v[r + 1][q] & ~(p4_pi(ln & rn) & u & d) & ~p4_pi(f);
+                    vs[q] = 0u;
+                } else {
+                    if (tail) fix_tail(pw0 + q, p, rn, f);
+                    const uint32_t u = top ? fw : cu[q];
+                    const uint32_t d = bot ? fw : cd[q];
+                    const uint32_t a = ln | rn | u | d;
+                    ve[q ^ SWAP] = cc[q] | ~a | f;
+                    vs[q ^ SWAP] = (~cc[q] & a) | f;
+                }
             }
             if (nst == CW && p.vst) {
                 if (OUT != kOutEset) store_chunk<CW>(p.o_edges + o, ve);

@@ -475,11 +475,16 @@ def count_black(words, width) -> torch.Tensor:
     return counts
 
 
-def scan_edges(words, width, border=WHITE_OUTSIDE):
+def scan_edges(words, width, border=WHITE_OUTSIDE, *, out=None):
     """detect_edges_scan: per-pixel Edge(p) on the device."""
     squeeze = words.dim() == 2
     w3, wb, rs = _packed(words, width)
-    o = _new_like(w3, squeeze)
+    if out is None:
+        o = _new_like(w3, squeeze)
+    else:
+        o = out
+        if _row_stride(_check_out(o, w3, squeeze), "out") != rs:
+            raise ValueError("out must have the input's row stride")
     n, h, _ = w3.shape
     _capi.call("be_scan_edges", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
                fill_bit(border), _stream(w3))

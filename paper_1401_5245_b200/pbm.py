@@ -107,14 +107,19 @@ def write_pbm(img: BitImage, raw: bool = True) -> bytes:
     return head + ("\n".join(lines) + "\n").encode()
 
 
-def detect_p4(payload, n: int, h: int, w: int, border=BorderPolicy.WHITE_OUTSIDE):
+def detect_p4(payload, n: int, h: int, w: int, border=BorderPolicy.WHITE_OUTSIDE, *, out=None):
     """Edges of a batch of P4 payloads already in HBM (uint8 tensor of
-    n * h * ceil(w/8) bytes) -> P4 payload tensor of the same size."""
+    n * h * ceil(w/8) bytes) -> P4 payload tensor of the same size (`out`, if
+    given: a contiguous CUDA uint8 tensor of that many bytes)."""
     torch = _torch()
     rb = (w + 7) // 8
     if payload.numel() != n * h * rb or payload.dtype != torch.uint8 or not payload.is_cuda:
         raise ValueError(f"payload must be a CUDA uint8 tensor of {n * h * rb} bytes")
-    out = torch.empty_like(payload)
+    if out is None:
+        out = torch.empty_like(payload)
+    elif (out.numel() != payload.numel() or out.dtype != torch.uint8 or not out.is_cuda
+          or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous CUDA uint8 tensor of {n * h * rb} bytes")
     scratch = None
     if rb % 16 != 0 or os.environ.get("BITEDGE_P4_UNFUSED"):   # general (3-pass) path
         scratch = torch.empty(2 * n * h * ((w + 31) // 32), dtype=torch.int32, device=payload.device)
