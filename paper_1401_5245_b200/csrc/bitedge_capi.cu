@@ -187,18 +187,25 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 // Launch helpers: dispatch the runtime choices onto template parameters.
 template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
-    if (!swap && rs == 2) {
-        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
-        else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
-    } else if (!swap && rs == 8) {
-        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp);
-        else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp);
-    } else if (swap) {
-        if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
-        else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
-    } else {
-        if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp);
+    if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
+        if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
         else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        (void)cw;
+    } else {
+        if (!swap && rs == 2) {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
+        } else if (!swap && rs == 8) {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp);
+        } else if (swap) {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        } else {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        }
     }
     return cuda_check("edge_reg_packed_kernel");
 }
@@ -215,9 +222,17 @@ int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
     return cuda_check("edge_reg_u8_kernel");
 }
 
+inline bool multi_out(const RegParams &rp) {
+    return rp.o_side[0] || rp.o_side[1] || rp.o_side[2] || rp.o_side[3] || rp.o_packed;
+}
+
 template <bool HALO>
 int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
                     cudaStream_t st) {
+    if (multi_out(rp)) {          // packed input only (uint8 multi-output goes to K2t2 or tile)
+        if (input_kind == 1) return 1;
+        return launch_reg_packed<kOutAll, HALO>(rp, swap, cw, rs, grid, st);
+    }
     if (input_kind == 1) {
         if (rp.o_edges && rp.o_eset) return launch_reg_u8<kOutAny, HALO>(rp, rs, grid, st);
         if (rp.o_eset) return launch_reg_u8<kOutEset, HALO>(rp, rs, grid, st);
@@ -232,8 +247,9 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
-            const void *below, uint32_t *o_edges, uint32_t *o_eset, int64_t out_stride_u32,
-            const Geometry &G, int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
+            const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
+            uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
+            int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
     const char *e = getenv("BITEDGE_KERNEL");
     if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return 1;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
@@ -244,6 +260,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     rp.in = (const char *)in; rp.above = (const char *)above; rp.below = (const char *)below;
     rp.in_row_bytes = in_row_bytes;
     rp.o_edges = o_edges; rp.o_eset = o_eset; rp.out_stride = out_stride_u32;
+    for (int k = 0; k < 4; ++k) rp.o_side[k] = o_side[k];
+    rp.o_packed = o_packed;
+    const bool multi = multi_out(rp);
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
@@ -256,15 +275,17 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // 5.3 / 79 % for 4-word x 4-row items; scripts/c3sweep.sh).
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
     const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
-    int cw = (input_kind == 0 && in32 && !getenv("BITEDGE_CW4")) ? 8 : 4;
+    int cw = (input_kind == 0 && in32 && !multi && !getenv("BITEDGE_CW4")) ? 8 : 4;
     const int packed_rs = (input_kind == 0 && !G.swap && !big) ? 2 : 4;
-    if (input_kind == 0 && in32 && getenv("BITEDGE_CW8")) cw = 8;
+    if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
     rp.thr = thr;
     const int ocw = input_kind == 1 ? 1 : cw;
     rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
-    if (input_kind == 1 && !above && !below && row_lo == 0 && row_hi == nrows &&
+    for (int k = 0; k < 4; ++k) rp.vst = rp.vst && al(o_side[k], 4 * ocw);
+    rp.vst = rp.vst && al(o_packed, 4 * ocw);
+    if (input_kind == 1 && !multi && !above && !below && row_lo == 0 && row_hi == nrows &&
         in_row_bytes == G.w && ((uintptr_t)in % 32) == 0 && G.w % 32 == 0 && G.wp <= 32 &&
         (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !getenv("BITEDGE_NO_WARPIMG")) {
         const int lwpr = ilog2(G.wp), rpi = 32 >> lwpr;
@@ -315,7 +336,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
     } while (0)
-            if (rp.o_edges && rp.o_eset) {
+            if (multi) {
+                if (halo) BE_TMA2(kOutAll, true); else BE_TMA2(kOutAll, false);
+            } else if (rp.o_edges && rp.o_eset) {
                 if (halo) BE_TMA2(kOutAny, true); else BE_TMA2(kOutAny, false);
             } else if (rp.o_eset) {
                 if (halo) BE_TMA2(kOutEset, true); else BE_TMA2(kOutEset, false);
@@ -326,6 +349,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             return cuda_check("edge_tma2_u8_kernel");
         }
     }
+    if (multi && input_kind == 1) return 1;          // other uint8 shapes: tile kernel
     if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
@@ -386,6 +410,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         const char *rse = getenv("BITEDGE_PRS");      // packed strip height experiments: 2/4/8
         if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
     }
+    if (multi && rs == 8) rs = 4;                    // kOutAll has 2- and 4-row strips
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
     const int64_t grid = (threads + kThreads - 1) / kThreads;
@@ -518,10 +543,10 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
         if (above && (rc = check_ptr(above, word_bits, "above halo"))) return rc;
         if (below && (rc = check_ptr(below, word_bits, "below halo"))) return rc;
         tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
+        rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset, o_side,
+                     o_packed, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
+        if (rc != 1) return rc;
         if (only_edges) {
-            rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
-                         tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
-            if (rc != 1) return rc;
             rc = try_stream(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
                             word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
             if (rc != 1) return rc;
@@ -536,10 +561,12 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     if (in_stride < w) return fail(BE_EINVAL, "input row stride %lld bytes < width %lld",
                                    (long long)in_stride, (long long)w);
     tp.in_stride = in_stride;
-    if (only_edges && word_bits == 32) {
-        rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, tp.out_stride, G, nrows,
-                     row_lo, row_hi, st, thr);
+    if (word_bits == 32) {
+        rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, o_side, o_packed,
+                     tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
         if (rc != 1) return rc;
+    }
+    if (only_edges && word_bits == 32) {
         rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
                         G, nrows, row_lo, row_hi, st, thr);
         if (rc != 1) return rc;

@@ -47,7 +47,22 @@ struct RegParams {
     int vst;                 // 128-bit output stores allowed
     int v8;                  // uint8 rows are 32-B aligned: 256-bit loads
     int thr;                 // uint8 pack threshold (1 = nonzero is white)
+    uint32_t *o_side[4];     // kOutAll only: fundamental edges L, R, U, D (or nullptr)
+    uint32_t *o_packed;      // kOutAll only: the packed input, padding 1 (or nullptr)
 };
+
+// kOutAll: every requested output of one word from the values the edge formula
+// already has (pixel-order, white polarity): centre c, the neighbour planes
+// ln / rn / u / d (fill applied) and the padding force f.  Fundamental edge of
+// a side = black centre AND white neighbour on that side.
+struct AllWords {
+    uint32_t e, s, l, r, u, d, pk;
+};
+__device__ __forceinline__ AllWords all_words(uint32_t c, uint32_t ln, uint32_t rn, uint32_t u,
+                                              uint32_t d, uint32_t f) {
+    const uint32_t a = ln | rn | u | d, b = ~c;
+    return {c | ~a | f, (b & a) | f, (b & ln) | f, (b & rn) | f, (b & u) | f, (b & d) | f, c | f};
+}
 
 template <int SWAP>
 __device__ __forceinline__ uint4 pix_order(uint4 v) {
@@ -174,6 +189,8 @@ edge_reg_packed_kernel(const RegParams p) {
             const bool top = (y == 0) && !(HALO && p.above);
             const bool bot = (y == p.h - 1) && !(HALO && p.below);
             uint32_t ve[CW], vs[CW];
+            constexpr int NA = OUT == kOutAll ? CW : 1;
+            uint32_t lnv[NA], rnv[NA], uv[NA], dv[NA], fv[NA];   // kOutAll only
 #pragma unroll
             for (int q = 0; q < CW; ++q) {
                 const uint32_t left = q == 0 ? lw : cc[q - 1];
@@ -199,9 +216,36 @@ edge_reg_packed_kernel(const RegParams p) {
                     const uint32_t a = ln | rn | u | d;
                     ve[q ^ SWAP] = cc[q] | ~a | f;
                     vs[q ^ SWAP] = (~cc[q] & a) | f;
+                    if (OUT == kOutAll) {
+                        lnv[q] = ln; rnv[q] = rn; uv[q] = u; dv[q] = d; fv[q] = f;
+                    }
                 }
             }
-            if (nst == CW && p.vst) {
+            if constexpr (OUT == kOutAll) {
+                // one output at a time, rebuilt from the neighbour planes
+                auto put = [&](uint32_t *dst, int which) {
+                    if (dst == nullptr) return;
+                    uint32_t t[CW];
+#pragma unroll
+                    for (int q = 0; q < CW; ++q) {
+                        const AllWords x = all_words(cc[q], lnv[q], rnv[q], uv[q], dv[q], fv[q]);
+                        t[q ^ SWAP] = which == 0 ? x.e : which == 1 ? x.s : which == 2 ? x.l
+                                    : which == 3 ? x.r : which == 4 ? x.u : which == 5 ? x.d : x.pk;
+                    }
+                    if (nst == CW && p.vst) {
+                        store_chunk<CW>(dst + o, t);
+                    } else {
+                        for (int q = 0; q < nst; ++q) dst[o + q] = t[q];
+                    }
+                };
+                put(p.o_edges, 0);
+                put(p.o_eset, 1);
+                put(p.o_side[0], 2);
+                put(p.o_side[1], 3);
+                put(p.o_side[2], 4);
+                put(p.o_side[3], 5);
+                put(p.o_packed, 6);
+            } else if (nst == CW && p.vst) {
                 if (OUT != kOutEset) store_chunk<CW>(p.o_edges + o, ve);
                 if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + o, vs);
             } else {
@@ -795,13 +839,28 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
             const uint32_t lnB = __funnelshift_r(xb, lwb, 1);
             const uint32_t rnB = (__funnelshift_l(rwb, xb, 1) & kb) | fb;
             const uint32_t anyB = lnB | rnB | uB | dB;
-            if (la) {
-                if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
-                if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
-            }
-            if (lb_) {
-                if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
-                if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
+            if (OUT == kOutAll) {
+                const AllWords A = all_words(xa, lnA, rnA, uA, dA, ga);
+                const AllWords B = all_words(xb, lnB, rnB, uB, dB, gb);
+                uint32_t *dst[7] = {p.o_edges, p.o_eset, p.o_side[0], p.o_side[1], p.o_side[2],
+                                    p.o_side[3], p.o_packed};
+                const uint32_t va[7] = {A.e, A.s, A.l, A.r, A.u, A.d, A.pk};
+                const uint32_t vb[7] = {B.e, B.s, B.l, B.r, B.u, B.d, B.pk};
+#pragma unroll
+                for (int k = 0; k < 7; ++k) {
+                    if (dst[k] == nullptr) continue;
+                    if (la) __stcs(dst[k] + o, va[k]);
+                    if (lb_) __stcs(dst[k] + o + 32, vb[k]);
+                }
+            } else {
+                if (la) {
+                    if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
+                }
+                if (lb_) {
+                    if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
+                }
             }
         }
     };

@@ -43,6 +43,7 @@ enum OutKind : int {
     kOutEdges = 0,     // detect_edges_mask only (the hot path)
     kOutEset = 1,      // EdgeSet only
     kOutAny = 2,       // any subset of the optional outputs
+    kOutAll = 3,       // register kernels: edges / EdgeSet / 4 sides / packed, each if non-null
 };
 
 struct TileParams {

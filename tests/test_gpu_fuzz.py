@@ -119,18 +119,25 @@ def test_fuzz_halo_slabs_all_inputs(knob, cuda_dev, monkeypatch):
             "u32": (torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev), 32),
             "u64": (torch.from_numpy(P.from_array(a).words.view(np.int64)).to(cuda_dev), 64),
         }
+        img = P.from_array(a)
+        mask = P.build_mask(img)
+        exp_all = {"edges": exp}
+        for k, d in (("left", P.LEFT), ("right", P.RIGHT), ("up", P.UP), ("down", P.DOWN)):
+            exp_all[k] = P.u64_to_u32_rows(P.fundamental_edge(img, mask, d, 1).words)[:, : -(-W // 32)]
         for name, (full, wb) in views.items():
-            parts = []
+            parts = {k: [] for k in exp_all}
             for lo, hi in zip(cuts[:-1], cuts[1:]):
                 slab = full[lo:hi].clone()
                 above = full[lo - 1].clone() if lo > 0 else None
                 below = full[hi].clone() if hi < H else None
                 res = cu.edges_general(slab.unsqueeze(0), W, 1, word_bits=wb, above=above,
-                                       below=below)
-                parts.append(res["edges"][0])
-            got = torch.cat(parts).cpu().numpy()
-            if wb == 64:
-                got = P.u64_to_u32_rows(got.view(np.uint64))[:, : -(-W // 32)]
-            else:
-                got = got.view(np.uint32)
-            assert (got == exp).all(), (knob, name, H, W, cuts)
+                                       below=below, sides=True)
+                for k in parts:
+                    parts[k].append(res[k][0])
+            for k, ex in exp_all.items():
+                got = torch.cat(parts[k]).cpu().numpy()
+                if wb == 64:
+                    got = P.u64_to_u32_rows(got.view(np.uint64))[:, : -(-W // 32)]
+                else:
+                    got = got.view(np.uint32)
+                assert (got == ex).all(), (knob, name, k, H, W, cuts)
