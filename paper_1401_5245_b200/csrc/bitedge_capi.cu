@@ -294,15 +294,27 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const int64_t nimg = G.n;
             const int64_t grid = (nimg * 32 + kThreads - 1) / kThreads;
             if (grid <= 0x7FFFFFFFLL) {
+#define BE_WARPIMG_G(L, GM)                                                                    \
+    do {                                                                                       \
+        if (o_edges && o_eset)                                                                 \
+            launch_k(edge_warp_img_kernel<L, kOutAny, GM>, (unsigned)grid, 0, st, rp, groups,  \
+                     nimg);                                                                    \
+        else if (o_eset)                                                                       \
+            launch_k(edge_warp_img_kernel<L, kOutEset, GM>, (unsigned)grid, 0, st, rp, groups, \
+                     nimg);                                                                    \
+        else                                                                                   \
+            launch_k(edge_warp_img_kernel<L, kOutEdges, GM>, (unsigned)grid, 0, st, rp,        \
+                     groups, nimg);                                                            \
+    } while (0)
 #define BE_WARPIMG(L)                                                                          \
     case L:                                                                                    \
-        if (o_edges && o_eset)                                                                 \
-            launch_k(edge_warp_img_kernel<L, kOutAny>, (unsigned)grid, 0, st, rp, groups, nimg); \
-        else if (o_eset)                                                                       \
-            launch_k(edge_warp_img_kernel<L, kOutEset>, (unsigned)grid, 0, st, rp, groups, nimg); \
-        else                                                                                   \
-            launch_k(edge_warp_img_kernel<L, kOutEdges>, (unsigned)grid, 0, st, rp, groups, nimg); \
+        if (groups <= 4 && !g8) BE_WARPIMG_G(L, 4); else BE_WARPIMG_G(L, 8);                   \
         return cuda_check("edge_warp_img_kernel");
+                // GMAX = 4 (48 regs, one wave of 4096 C2 images) is 1.5 % faster with
+                // overlapped batches but 9 % slower serially under PDL than GMAX = 8
+                // (77 regs, 1.15 waves): opt-in knob.
+                const bool g8 = getenv("BITEDGE_WARPIMG_G4") == nullptr;
+                rp.pdl_late = getenv("BITEDGE_PDL_LATE") != nullptr;
                 switch (lwpr) {
                     BE_WARPIMG(0)
                     BE_WARPIMG(1)
@@ -313,6 +325,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                     default: break;
                 }
 #undef BE_WARPIMG
+#undef BE_WARPIMG_G
             }
         }
     }

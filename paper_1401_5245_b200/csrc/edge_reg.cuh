@@ -49,6 +49,7 @@ struct RegParams {
     int thr;                 // uint8 pack threshold (1 = nonzero is white)
     uint32_t *o_side[4];     // kOutAll only: fundamental edges L, R, U, D (or nullptr)
     uint32_t *o_packed;      // kOutAll only: the packed input, padding 1 (or nullptr)
+    int pdl_late;            // K2w: signal dependents after the stores, not at entry
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -314,12 +315,14 @@ __device__ __forceinline__ void ldg_stream_v8(const void *p, uint4 &a, uint4 &b)
 // Up/down neighbours come from lane -/+ WPR (or the adjacent row group's
 // register), left/right from lane -/+ 1; no halo rows are loaded because an
 // image's outer neighbours are the border fill.  Requires w == 32 * WPR,
-// contiguous rows, h == G * RPI with G <= 8.
-template <int LWPR, int OUT>
+// contiguous rows, h == G * RPI with G <= GMAX <= 8.  GMAX sizes the register
+// file for the up-front loads: C2 (G = 4) with GMAX = 4 needs ~half the
+// registers of GMAX = 8, so more warps are resident -- 4096 images in one wave.
+template <int LWPR, int OUT, int GMAX = 8>
 __global__ void __launch_bounds__(kThreads)
 edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
     pdl_wait();
-    pdl_trigger();
+    if (!p.pdl_late) pdl_trigger();
     const Thr T = make_thr(p.thr);
     constexpr int WPR = 1 << LWPR;
     constexpr int RPI = 32 >> LWPR;
@@ -329,19 +332,19 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
     const int rl = lane >> LWPR, wi = lane & (WPR - 1);
     const uint32_t fw = p.fillword;
     const char *src = p.in + img * (int64_t)G * 1024 + 32 * lane;
-    uint4 a[8], b[8];
+    uint4 a[GMAX], b[GMAX];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < GMAX; ++k)
         if (k < G) ldg_stream_v8(src + 1024 * k, a[k], b[k]);
-    uint32_t wd[8];
+    uint32_t wd[GMAX];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) wd[k] = k < G ? pack32_any(a[k], b[k], T) : 0xFFFFFFFFu;
+    for (int k = 0; k < GMAX; ++k) wd[k] = k < G ? pack32_any(a[k], b[k], T) : 0xFFFFFFFFu;
 
     uint32_t *oe = p.o_edges + img * (int64_t)G * 32 + lane;
     uint32_t *os = p.o_eset + img * (int64_t)G * 32 + lane;
     const bool last_word = (wi == WPR - 1);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < GMAX; ++k) {
         if (k >= G) break;
         const uint32_t cw = wd[k];
         // rows above / below inside this row group, and across the group boundary
@@ -349,7 +352,8 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
         const uint32_t dn_in = __shfl_down_sync(0xFFFFFFFFu, cw, WPR);
         const uint32_t up_x = __shfl_sync(0xFFFFFFFFu, k > 0 ? wd[k > 0 ? k - 1 : 0] : fw,
                                           (lane + 32 - WPR) & 31);
-        const uint32_t dn_x = __shfl_sync(0xFFFFFFFFu, k + 1 < G ? wd[k + 1 < 8 ? k + 1 : 7] : fw,
+        const uint32_t dn_x = __shfl_sync(0xFFFFFFFFu,
+                                          k + 1 < G ? wd[k + 1 < GMAX ? k + 1 : GMAX - 1] : fw,
                                           (lane + WPR) & 31);
         const uint32_t u = rl > 0 ? up_in : (k > 0 ? up_x : fw);
         const uint32_t d = rl < RPI - 1 ? dn_in : (k + 1 < G ? dn_x : fw);
@@ -363,6 +367,7 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
         if (OUT != kOutEset) __stcs(oe + 32 * k, cw | ~any);
         if (OUT != kOutEdges) __stcs(os + 32 * k, ~cw & any);
     }
+    if (p.pdl_late) pdl_trigger();
 }
 
 template <int RS, int OUT, bool HALO, bool V8>

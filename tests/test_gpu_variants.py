@@ -29,6 +29,8 @@ VARIANTS = {
     "tma_warp": {"BITEDGE_FORCE_TMA": "1"},
     "tma_warp1k": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA1": "1"},
     "no_tma": {"BITEDGE_NO_TMA": "1"},
+    "warpimg_g4": {"BITEDGE_WARPIMG_G4": "1"},
+    "pdl_late": {"BITEDGE_PDL_LATE": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
