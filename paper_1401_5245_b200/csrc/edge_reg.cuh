@@ -118,7 +118,7 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
 __device__ __forceinline__ uint32_t p4_pi(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
 template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false>
-__global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 1)   // P4: 3 (4-row) or 4 CTAs/SM
+__global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
 edge_reg_packed_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
