@@ -282,10 +282,12 @@ __device__ __forceinline__ uint32_t pack8_01(uint32_t x, uint32_t y) {
 // normalisation; any other byte value takes the general path.  Exact for all
 // inputs (nonzero -> white, bitimage.py:124,133).
 __device__ __forceinline__ uint32_t pack32_any(uint4 a, uint4 b, const Thr &T) {
-    const uint32_t hi = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
-    if (hi == 0u && T.t == 1u) {
-        return (pack8_01(a.x, a.y) << 24) | (pack8_01(a.z, a.w) << 16) |
-               (pack8_01(b.x, b.y) << 8) | pack8_01(b.z, b.w);
+    if (T.t == 1u) {     // launch-uniform: thresholded launches skip the 0/1 test
+        const uint32_t hi = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
+        if (hi == 0u) {
+            return (pack8_01(a.x, a.y) << 24) | (pack8_01(a.z, a.w) << 16) |
+                   (pack8_01(b.x, b.y) << 8) | pack8_01(b.z, b.w);
+        }
     }
     return pack32(a, b, T);
 }

@@ -111,7 +111,7 @@ __device__ __forceinline__ Thr make_thr(int t) {
 // no-borrow bit of ((bl | 0x80) - tl); then ge = bh | that (t < 128) or
 // bh & that (t >= 128), one LOP3 either way.  For t = 1 this is "byte != 0".
 __device__ __forceinline__ uint32_t ge_bytes(uint32_t v, const Thr &T) {
-    const uint32_t x = ((v & 0x7F7F7F7Fu) | 0x80808080u) - T.tl;
+    const uint32_t x = (v | 0x80808080u) - T.tl;     // == ((v & 0x7F..) | 0x80..) - tl
     return ((v & x) | (T.m & (v | x))) & 0x80808080u;
 }
 
