@@ -168,6 +168,7 @@ edge_reg_packed_kernel(const RegParams p) {
 
     const bool tail = pw0 + CW - 1 >= p.pl;
     const int nst = min(CW, p.wp - pw0);
+    const uint32_t pad_pi = P4 ? p4_pi(p.padmask) : 0u;
     uint32_t y = live ? (uint32_t)(g0 % p.h) : 0u;
     int64_t o = g0 * p.out_stride + pw0;
 #pragma unroll
@@ -200,15 +201,21 @@ edge_reg_packed_kernel(const RegParams p) {
                 uint32_t rn = __funnelshift_l(right, cc[q], 1);
                 uint32_t f = 0u;
                 if (P4) {
-                    // ln / rn are ~Ln / ~Rn here (black polarity)
+                    // ln / rn are ~Ln / ~Rn here (black polarity); the padding force
+                    // is applied in the P4 byte order directly (pad_pi = pi(padmask))
+                    uint32_t fpi = 0u;
                     if (tail) {
-                        uint32_t rw_ = ~rn;
-                        fix_tail(pw0 + q, p, rw_, f);
-                        rn = ~rw_;
+                        const int pw = pw0 + q;
+                        if (pw == p.pl) {
+                            rn = (rn & ~p.lastbit) | (~fw & p.lastbit);
+                            fpi = pad_pi;
+                        } else if (pw > p.pl) {
+                            fpi = 0xFFFFFFFFu;
+                        }
                     }
                     const uint32_t u = top ? ~fw : cu[q];
                     const uint32_t d = bot ? ~fw : cd[q];
-                    ve[q] = v[r + 1][q] & ~(p4_pi(ln & rn) & u & d) & ~p4_pi(f);
+                    ve[q] = v[r + 1][q] & ~(p4_pi(ln & rn) & u & d) & ~fpi;
                     vs[q] = 0u;
                 } else {
                     if (tail) fix_tail(pw0 + q, p, rn, f);
