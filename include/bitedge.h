@@ -189,6 +189,16 @@ int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64
                   int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
                   int64_t chunk_images, void *stream0, void *stream1, int blocking);
 
+/* The same for ONE large host image, chunked by rows (C3 / C4-sized rasters,
+ * where image chunks would leave nothing to overlap): chunk c copies rows
+ * [r0 - 1, r1 + 1) in (the 1-row halos), computes rows [r0, r1) with the halo
+ * kernel and copies them out, on stream (c % 2).  dev_in[i] >= (chunk_rows + 2)
+ * input rows, dev_out[i] >= chunk_rows output rows.  Input rows are w bytes
+ * (input_kind 1) or ceil(w/32) uint32 words (input_kind 0). */
+int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
+                       int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
+                       int64_t chunk_rows, void *stream0, void *stream1, int blocking);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);
 int be_abi_version(void);

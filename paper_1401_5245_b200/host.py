@@ -26,7 +26,7 @@ class HostBatchEdges:
     directions and the kernels overlap without any per-chunk Python work."""
 
     def __init__(self, shape, kind: str = "u8", width: int | None = None, border=1,
-                 chunk_images: int | None = None, device=None):
+                 chunk_images: int | None = None, device=None, chunk_rows: int | None = None):
         if kind not in ("u8", "packed"):
             raise ValueError("kind must be 'u8' or 'packed'")
         self.device = torch.device(device) if device is not None else torch.device(
@@ -40,14 +40,30 @@ class HostBatchEdges:
         self.in_dtype = torch.uint8 if kind == "u8" else torch.int32
         self.in_shape = (n, h, s)
         self.out_shape = (n, h, cu.words_per_row(self.width, 32))
-        if chunk_images is None:
-            per_img = h * s * (1 if kind == "u8" else 4)
-            chunk_images = max(1, min(n, (8 << 20) // max(1, per_img)))    # ~8 MiB per chunk
-        self.chunk = int(chunk_images)
-        self.d_in = [torch.empty((self.chunk, h, s), dtype=self.in_dtype, device=self.device)
-                     for _ in range(2)]
-        self.d_out = [torch.empty((self.chunk,) + self.out_shape[1:], dtype=torch.int32,
-                                  device=self.device) for _ in range(2)]
+        row_bytes = s * (1 if kind == "u8" else 4)
+        per_img = h * row_bytes
+        # a single image of >= 4 MiB: chunk it by rows (1-row halos; >= 4 chunks of
+        # <= 8 MiB) so its copies overlap the kernels (be_host_edges_rows)
+        self.rows_mode = n == 1 and chunk_images is None and (
+            chunk_rows is not None or per_img >= (4 << 20))
+        if chunk_rows is not None and not self.rows_mode:
+            raise ValueError("chunk_rows applies to a single image (n == 1)")
+        if self.rows_mode:
+            if chunk_rows is None:
+                chunk_rows = max(1, min(8 << 20, per_img // 4) // row_bytes)
+            self.chunk = int(chunk_rows)                                    # rows per chunk
+            self.d_in = [torch.empty((self.chunk + 2, s), dtype=self.in_dtype, device=self.device)
+                         for _ in range(2)]
+            self.d_out = [torch.empty((self.chunk, self.out_shape[2]), dtype=torch.int32,
+                                      device=self.device) for _ in range(2)]
+        else:
+            if chunk_images is None:
+                chunk_images = max(1, min(n, (8 << 20) // max(1, per_img)))  # ~8 MiB per chunk
+            self.chunk = int(chunk_images)
+            self.d_in = [torch.empty((self.chunk, h, s), dtype=self.in_dtype, device=self.device)
+                         for _ in range(2)]
+            self.d_out = [torch.empty((self.chunk,) + self.out_shape[1:], dtype=torch.int32,
+                                      device=self.device) for _ in range(2)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(2)]
         self.h2d_bytes = n * h * s * (1 if kind == "u8" else 4)
         self.d2h_bytes = n * self.out_shape[1] * self.out_shape[2] * 4
@@ -73,6 +89,12 @@ class HostBatchEdges:
 
     def _run(self, host_in, host_out, blocking: bool) -> None:
         P = ctypes.c_void_p
+        if self.rows_mode:
+            _capi.call("be_host_edges_rows", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
+                       P(host_out.data_ptr()), self.h, self.width, cu.fill_bit(self.border),
+                       self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
+                       P(self.streams[1].cuda_stream), 1 if blocking else 0)
+            return
         _capi.call("be_host_edges", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                    P(host_out.data_ptr()), self.n, self.h, self.width, cu.fill_bit(self.border),
                    self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),

@@ -75,3 +75,33 @@ for chunk in (4096, 2048, 1024, 512, 256):
     ms2 = timed(step_submit)
     print(f"HostBatchEdges chunk={chunk}: __call__ {ms:.4f} ms/step -> {4096 * 4096 / ms / 1e6:.1f} "
           f"Gpx/s; submit {ms2:.4f} ms/step -> {4096 * 4096 / ms2 / 1e6:.1f} Gpx/s")
+
+# C4-sized: 512 MiB in and 512 MiB out, 8 MiB chunks, both directions at once
+big_in = torch.empty(512 << 20, dtype=torch.uint8, pin_memory=True)
+big_out = torch.empty(512 << 20, dtype=torch.uint8, pin_memory=True)
+dbuf = [torch.empty(8 << 20, dtype=torch.uint8, device=dev) for _ in range(2)]
+dsrc = torch.empty(8 << 20, dtype=torch.uint8, device=dev)
+ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+
+def duplex(_):
+    for c in range(64):
+        with torch.cuda.stream(ss[c & 1]):
+            dbuf[c & 1].copy_(big_in[c << 23:(c + 1) << 23], non_blocking=True)
+            big_out[c << 23:(c + 1) << 23].copy_(dsrc, non_blocking=True)
+
+
+def h2d_only_big(_):
+    for c in range(64):
+        with torch.cuda.stream(ss[c & 1]):
+            dbuf[c & 1].copy_(big_in[c << 23:(c + 1) << 23], non_blocking=True)
+
+
+def d2h_only_big(_):
+    for c in range(64):
+        with torch.cuda.stream(ss[c & 1]):
+            big_out[c << 23:(c + 1) << 23].copy_(dsrc, non_blocking=True)
+
+
+print(f"512 MiB H2D only: {timed(h2d_only_big, 5):.3f} ms; D2H only: {timed(d2h_only_big, 5):.3f} ms; "
+      f"both at once: {timed(duplex, 5):.3f} ms")

@@ -388,6 +388,39 @@ def test_host_pipeline_submit(cuda_dev):
     assert pend[0].query() and pend[1].query()
 
 
+@pytest.mark.parametrize("kind", ["u8", "packed"])
+@pytest.mark.parametrize("fill", [1, 0])
+def test_host_pipeline_rows(kind, fill, cuda_dev):
+    """A single host image chunked by rows (be_host_edges_rows): chunk sizes that
+    do and do not divide the height, 1-row chunks, and the automatic choice."""
+    import torch
+
+    from paper_1401_5245_b200 import synth
+    from paper_1401_5245_b200.host import HostBatchEdges
+
+    rng = np.random.default_rng(fill + (kind == "u8"))
+    for h, w in [(101, 2048), (37, 100), (64, 8192), (5, 33)]:
+        a = (rng.random((1, h, w)) < 0.5).astype(np.uint8)
+        exp = cscan.scan_u8(a, fill)
+        if kind == "u8":
+            host = torch.from_numpy(a * rng.integers(1, 256, a.shape).astype(np.uint8))
+        else:
+            host = torch.from_numpy(P.pack_u32(a).view(np.int32))
+        for cr in (1, 7, 16, h, None):
+            pipe = HostBatchEdges(tuple(host.shape), kind=kind, width=w, border=fill,
+                                  chunk_rows=cr)
+            hin, hout = pipe.new_host_buffers()
+            hin.copy_(host)
+            got = pipe(hin, hout).numpy().view(np.uint32)
+            assert (got == exp).all(), (kind, fill, h, w, cr)
+            assert pipe.rows_mode == (cr is not None)
+    big = synth.c3_words(h=4096)                                     # 4 MiB: automatic rows mode
+    pipe = HostBatchEdges((1, 4096, 256), kind="packed", width=8192, border=fill)
+    assert pipe.rows_mode
+    hin = torch.from_numpy(big.view(np.int32)).reshape(1, 4096, 256).pin_memory()
+    assert (pipe(hin).numpy().view(np.uint32)[0] == cscan.scan_p32(big, 8192, fill)).all()
+
+
 def test_fill_policies_on_border_touching_figure(cuda_dev):
     """Interior invariance: pixels >= 2 from the border do not depend
     on the policy; border pixels do."""
