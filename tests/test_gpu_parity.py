@@ -311,6 +311,69 @@ def test_config_c5_sample(cuda_dev):
     assert int(((~out) & packed).count_nonzero()) == 0
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("knob", [{}, {"BITEDGE_NO_TMA": "1"}, {"BITEDGE_KERNEL": "tile"}],
+                         ids=["default", "no_tma", "tile"])
+def test_beyond_4gib_offsets(knob, cuda_dev, monkeypatch):
+    """A uint8 raster of 4.4 GB (> 2^32 bytes, 2^32 pixels) and its packed form:
+    64-bit offsets everywhere.  Oracle on bands at the start, across the 2^31
+    and 2^32 byte marks and at the end (each band with its 1-row halos)."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    for k, v in knob.items():
+        monkeypatch.setenv(k, v)
+    h, w = 40000, 110016
+    g = torch.Generator(device=cuda_dev).manual_seed(11)
+    pix = (torch.rand((h, w), device=cuda_dev, generator=g) < 0.5).to(torch.uint8)
+    out = cu.pack_edges_u8(pix, 1)
+    packed = cu.pack_u8(pix)
+    assert torch.equal(cu.edges_packed(packed, w, 1), out)
+    for r in (0, (1 << 31) // w, (1 << 32) // w, h - 6):
+        lo, hi = max(0, r - 1), min(h, r + 7)
+        band = pix[lo:hi].cpu().numpy()[None]
+        exp = cscan.scan_u8(band, 1)[0]
+        got = _u32(out[lo:hi])
+        # interior rows of the band (its first/last row saw the band border)
+        a = 0 if lo == 0 else 1
+        b = hi - lo if hi == h else hi - lo - 1
+        assert (got[a:b] == exp[a:b]).all(), (knob, r)
+    del pix, out, packed
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("wb", [32, 64])
+def test_beyond_4gib_packed(wb, cuda_dev):
+    """A packed raster of 5.2 GB (40000 rows of 2^20 pixels) through K1."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    h, w = 40000, 1 << 20
+    dt = torch.int32 if wb == 32 else torch.int64
+    words = torch.randint(-2 ** 31, 2 ** 31 - 1, (h, w // 32), dtype=torch.int32,
+                          device=cuda_dev, generator=torch.Generator(device=cuda_dev).manual_seed(5))
+    inp = words if wb == 32 else words.view(torch.int64)
+    out = cu.edges_packed(inp, w, 1)
+    for r in (0, (1 << 31) // (w // 8), (1 << 32) // (w // 8), h - 6):
+        lo, hi = max(0, r - 1), min(h, r + 7)
+        band = words[lo:hi].cpu().numpy().view(np.uint32)
+        o = out[lo:hi].cpu().numpy()
+        if wb == 32:
+            band_px, got = band, o.view(np.uint32)
+        else:       # u64 words: pixel word p sits at u32 index p ^ 1
+            band_px = P.u64_to_u32_rows(band.view(np.uint64))
+            got = P.u64_to_u32_rows(o.view(np.uint64))
+        exp = cscan.scan_p32(band_px, w, 1)
+        a = 0 if lo == 0 else 1
+        b = hi - lo if hi == h else hi - lo - 1
+        assert (got[a:b] == exp[a:b]).all(), (wb, r)
+    del words, inp, out
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- row sharding (K3)
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
