@@ -518,53 +518,68 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         if shard == "rows" and world > 1:
-            e2e = None  # the row-sharded job's e2e needs host halos; reported at N=1 only
+            # this rank's row slab from host memory, with the neighbours'
+            # boundary rows as host halos (be_host_edges_rows)
+            from paper_1401_5245_b200 import synth
+
+            ha, hb = lo > 0, hi < h
+            pipe = HostBatchEdges(tuple(base.shape), kind=kind, width=w, device=dev,
+                                  halo_rows=(ha, hb))
+            hin, hout = pipe.new_host_buffers()
+            host_rows = synth.c4_slab(lo - ha, hi + hb, synth.c4_disks(), device=dev)
+            hin.copy_(host_rows.cpu().unsqueeze(0))
+            del host_rows
         else:
             pipe = HostBatchEdges(tuple(base.shape), kind=kind, width=w, device=dev)
             hin, hout = pipe.new_host_buffers()
             hin.copy_(base.cpu())
-            e2e_steps = max(3, min(steps, int(max(1, 2e9 / max(1, pipe.h2d_bytes)))))
-            houts = [hout, torch.empty_like(hout, pin_memory=True)]
-            for _ in range(2):
-                pipe(hin, hout)
-            # warm the pipelined (submit) path over both host output buffers for
-            # >= 0.25 s: a fresh box's first ~100 ms of PCIe traffic runs slower
-            t_w, k, pw = time.time(), 0, [None, None]
-            while k < 8 or time.time() - t_w < 0.25:
-                pw[k & 1] = pipe.submit(hin, houts[k & 1])
-                if k > 0:
-                    pw[(k - 1) & 1].synchronize()
-                k += 1
-            pw[(k - 1) & 1].synchronize()
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            # step i is submitted before step i-1's result is awaited and read on
-            # the host (two host output buffers), so the CPU-side sync latency of
-            # one step and its last chunk's kernel + D2H hide behind the next
-            # step's H2D (HostBatchEdges.submit does not chain batches)
-            pend = [None, None]
-            e0.record()
-            e0.synchronize()                     # every submitted copy starts after e0
-            for i in range(e2e_steps):
-                pend[i & 1] = pipe.submit(hin, houts[i & 1])
-                if i > 0:
-                    res = pend[(i - 1) & 1].synchronize()
-                    _ = int(res[0, 0, 0])        # step i-1's result, on the host
-            res = pend[(e2e_steps - 1) & 1].synchronize()
-            _ = int(res[0, 0, 0])
-            e1.record()
-            torch.cuda.synchronize()
-            ems = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([ems], device=dev, dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ems = float(t.item())
-            px_e2e = px_all
-            e2e = {"value": px_e2e * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gpixel/s",
-                   "h2d_bytes_per_step": int(pipe.h2d_bytes), "d2h_bytes_per_step":
-                   int(pipe.d2h_bytes), "steps": e2e_steps, "ms_per_step": ems / e2e_steps}
+        e2e_steps = max(3, min(steps, int(max(1, 2e9 / max(1, pipe.h2d_bytes)))))
+        houts = [hout, torch.empty_like(hout, pin_memory=True)]
+        for _ in range(2):
+            pipe(hin, hout)
+        # warm the pipelined (submit) path over both host output buffers for
+        # >= 0.25 s: a fresh box's first ~100 ms of PCIe traffic runs slower
+        t_w, k, pw = time.time(), 0, [None, None]
+        while k < 8 or time.time() - t_w < 0.25:
+            pw[k & 1] = pipe.submit(hin, houts[k & 1])
+            if k > 0:
+                pw[(k - 1) & 1].synchronize()
+            k += 1
+        pw[(k - 1) & 1].synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # step i is submitted before step i-1's result is awaited and read on
+        # the host (two host output buffers), so the CPU-side sync latency of
+        # one step and its last chunk's kernel + D2H hide behind the next
+        # step's H2D (HostBatchEdges.submit does not chain batches)
+        pend = [None, None]
+        e0.record()
+        e0.synchronize()                     # every submitted copy starts after e0
+        for i in range(e2e_steps):
+            pend[i & 1] = pipe.submit(hin, houts[i & 1])
+            if i > 0:
+                res = pend[(i - 1) & 1].synchronize()
+                _ = int(res[0, 0, 0])        # step i-1's result, on the host
+        res = pend[(e2e_steps - 1) & 1].synchronize()
+        _ = int(res[0, 0, 0])
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        px_e2e = px_all
+        moved = [int(pipe.h2d_bytes), int(pipe.d2h_bytes)]
+        if world > 1:                        # the whole job's bytes per step
+            t = torch.tensor(moved, device=dev, dtype=torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            moved = [int(v) for v in t.tolist()]
+        e2e = {"value": px_e2e * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gpixel/s",
+               "h2d_bytes_per_step": moved[0], "d2h_bytes_per_step": moved[1],
+               "steps": e2e_steps, "ms_per_step": ems / e2e_steps}
 
     # ---- parity gate on the measured output (before reporting a number)
     parity = None

@@ -189,15 +189,19 @@ int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64
                   int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
                   int64_t chunk_images, void *stream0, void *stream1, int blocking);
 
-/* The same for ONE large host image, chunked by rows (C3 / C4-sized rasters,
- * where image chunks would leave nothing to overlap): chunk c copies rows
- * [r0 - 1, r1 + 1) in (the 1-row halos), computes rows [r0, r1) with the halo
- * kernel and copies them out, on stream (c % 2).  dev_in[i] >= (chunk_rows + 2)
- * input rows, dev_out[i] >= chunk_rows output rows.  Input rows are w bytes
- * (input_kind 1) or ceil(w/32) uint32 words (input_kind 0). */
+/* The same for ONE large host image (or one row slab of it), chunked by rows
+ * (C3 / C4-sized rasters, where image chunks would leave nothing to overlap):
+ * chunk c copies rows [r0 - 1, r1 + 1) in (the 1-row halos), computes rows
+ * [r0, r1) with the halo kernel and copies them out, on stream (c % 2).
+ * dev_in[i] >= (chunk_rows + 2) input rows, dev_out[i] >= chunk_rows output
+ * rows.  Input rows are w bytes (input_kind 1) or ceil(w/32) uint32 words
+ * (input_kind 0).  halo_flags: bit 0 = host_in starts with row -1 (the row
+ * above a slab), bit 1 = it ends with row h; without them the border fill
+ * applies there.  host_out receives rows 0 .. h-1. */
 int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
-                       int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
-                       int64_t chunk_rows, void *stream0, void *stream1, int blocking);
+                       int64_t w, int fill_bit, int halo_flags, void *const dev_in[2],
+                       uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,
+                       void *stream1, int blocking);
 
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);

@@ -54,7 +54,7 @@ _SIGNATURES = {
     "be_ipc_close": [_P, _I64],
     "be_host_edges": [_P, _INT, _P, _I64, _I64, _I64, _INT, ctypes.POINTER(_P),
                       ctypes.POINTER(_P), _I64, _P, _P, _INT],
-    "be_host_edges_rows": [_P, _INT, _P, _I64, _I64, _INT, ctypes.POINTER(_P),
+    "be_host_edges_rows": [_P, _INT, _P, _I64, _I64, _INT, _INT, ctypes.POINTER(_P),
                            ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_last_error": [],
     "be_abi_version": [],

@@ -1180,8 +1180,9 @@ int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64
 }
 
 int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
-                       int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
-                       int64_t chunk_rows, void *stream0, void *stream1, int blocking) {
+                       int64_t w, int fill_bit, int halo_flags, void *const dev_in[2],
+                       uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,
+                       void *stream1, int blocking) {
     Geometry G;
     int rc = make_geometry(G, 32, 1, h, w, fill_bit);
     if (rc) return rc;
@@ -1191,24 +1192,29 @@ int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, 
     if (input_kind != 0 && input_kind != 1)
         return fail(BE_EINVAL, "input_kind must be 0 (packed u32) or 1 (uint8)");
     if (chunk_rows < 1) return fail(BE_EINVAL, "chunk_rows must be >= 1");
+    if (halo_flags & ~3) return fail(BE_EINVAL, "halo_flags must be a combination of 1 and 2");
     const int64_t wp = G.wp;
     const size_t in_row = input_kind == 1 ? (size_t)w : (size_t)wp * 4;
     const size_t out_row = (size_t)wp * 4;
+    const bool has_above = halo_flags & 1, has_below = halo_flags & 2;
+    // row r of the image is host row r + has_above; rows -1 / h exist iff flagged
+    const char *hin = (const char *)host_in + (has_above ? in_row : 0);
     cudaStream_t ss[2] = {S(stream0), S(stream1)};
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
     // chunk c on stream c % 2: H2D of rows [r0-1, r1+1) -> halo kernel on rows
     // [r0, r1) -> D2H; in-stream order protects buffer c % 2 for chunk c + 2
     for (int64_t c = 0, r0 = 0; r0 < h; ++c, r0 += chunk_rows) {
         const int64_t r1 = (h - r0) < chunk_rows ? h : r0 + chunk_rows;
-        const int64_t lo = r0 > 0 ? r0 - 1 : 0, hi = r1 < h ? r1 + 1 : h;
+        const bool up = r0 > 0 || has_above, dn = r1 < h || has_below;
+        const int64_t lo = up ? r0 - 1 : r0, hi = dn ? r1 + 1 : r1;
         const int b = (int)(c & 1);
         char *din = (char *)dev_in[b];
-        cudaError_t e = cudaMemcpyAsync(din, (const char *)host_in + lo * in_row, (hi - lo) * in_row,
+        cudaError_t e = cudaMemcpyAsync(din, hin + lo * (int64_t)in_row, (hi - lo) * in_row,
                                         cudaMemcpyHostToDevice, ss[b]);
         if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
         const char *slab = din + (r0 - lo) * in_row;
-        const void *above = r0 > 0 ? (const void *)din : nullptr;
-        const void *below = r1 < h ? (const void *)(slab + (r1 - r0) * in_row) : nullptr;
+        const void *above = up ? (const void *)din : nullptr;
+        const void *below = dn ? (const void *)(slab + (r1 - r0) * in_row) : nullptr;
         rc = edges_impl(slab, input_kind, input_kind == 1 ? w : wp, above, below, dev_out[b],
                         nullptr, side, nullptr, 32, wp, 1, r1 - r0, w, fill_bit, 0, r1 - r0, ss[b]);
         if (rc) return rc;

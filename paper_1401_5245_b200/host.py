@@ -26,7 +26,11 @@ class HostBatchEdges:
     directions and the kernels overlap without any per-chunk Python work."""
 
     def __init__(self, shape, kind: str = "u8", width: int | None = None, border=1,
-                 chunk_images: int | None = None, device=None, chunk_rows: int | None = None):
+                 chunk_images: int | None = None, device=None, chunk_rows: int | None = None,
+                 halo_rows: tuple = (False, False)):
+        """`halo_rows=(above, below)`: the host input of a single-image row slab
+        also holds the row above its first row / below its last row (a row shard
+        of a larger raster, multi-GPU); the result covers the slab's own rows."""
         if kind not in ("u8", "packed"):
             raise ValueError("kind must be 'u8' or 'packed'")
         self.device = torch.device(device) if device is not None else torch.device(
@@ -38,14 +42,17 @@ class HostBatchEdges:
             raise ValueError("packed host rows must hold exactly ceil(width/32) words")
         self.border = border
         self.in_dtype = torch.uint8 if kind == "u8" else torch.int32
-        self.in_shape = (n, h, s)
+        self.halo_flags = (1 if halo_rows[0] else 0) | (2 if halo_rows[1] else 0)
+        if self.halo_flags and n != 1:
+            raise ValueError("halo_rows apply to a single image (n == 1)")
+        self.in_shape = (n, h + bool(halo_rows[0]) + bool(halo_rows[1]), s)
         self.out_shape = (n, h, cu.words_per_row(self.width, 32))
         row_bytes = s * (1 if kind == "u8" else 4)
         per_img = h * row_bytes
         # a single image of >= 4 MiB: chunk it by rows (1-row halos; >= 4 chunks of
         # <= 8 MiB) so its copies overlap the kernels (be_host_edges_rows)
         self.rows_mode = n == 1 and chunk_images is None and (
-            chunk_rows is not None or per_img >= (4 << 20))
+            chunk_rows is not None or per_img >= (4 << 20) or self.halo_flags != 0)
         if chunk_rows is not None and not self.rows_mode:
             raise ValueError("chunk_rows applies to a single image (n == 1)")
         if self.rows_mode:
@@ -66,6 +73,10 @@ class HostBatchEdges:
                                       device=self.device) for _ in range(2)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(2)]
         self.h2d_bytes = n * h * s * (1 if kind == "u8" else 4)
+        if self.rows_mode:          # + the halo rows each chunk copies in
+            chunks = -(-h // self.chunk)
+            extra = 2 * (chunks - 1) + bool(self.halo_flags & 1) + bool(self.halo_flags & 2)
+            self.h2d_bytes += extra * row_bytes
         self.d2h_bytes = n * self.out_shape[1] * self.out_shape[2] * 4
         P = ctypes.c_void_p
         self._din = (P * 2)(*[t.data_ptr() for t in self.d_in])
@@ -92,7 +103,7 @@ class HostBatchEdges:
         if self.rows_mode:
             _capi.call("be_host_edges_rows", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                        P(host_out.data_ptr()), self.h, self.width, cu.fill_bit(self.border),
-                       self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
+                       self.halo_flags, self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
                        P(self.streams[1].cuda_stream), 1 if blocking else 0)
             return
         _capi.call("be_host_edges", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,

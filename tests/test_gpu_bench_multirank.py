@@ -24,7 +24,7 @@ def _port():
 
 
 @pytest.mark.parametrize("extra", [["--config", "c2", "--steps", "300"],
-                                   ["--config", "c4", "--steps", "4", "--no-e2e"],
+                                   ["--config", "c4", "--steps", "4"],
                                    ["--config", "c4", "--steps", "4", "--no-e2e", "--halo", "nccl"]],
                          ids=["c2-batch", "c4-rows-p2p", "c4-rows-nccl"])
 def test_bench_two_ranks_one_gpu(extra, cuda_dev):
@@ -42,5 +42,7 @@ def test_bench_two_ranks_one_gpu(extra, cuda_dev):
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["parity"]["ok"]
     if "c4" in extra:
         assert d["scaling"] == "strong" and "p2p" in d["config"]["parallelism"]
+        # e2e of the row shards (host halos): both ranks' slabs plus their halo rows
+        assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > (65536 * 2048 * 4)
     else:
         assert d["scaling"] == "weak" and d["config"]["global_batch"] == 8192

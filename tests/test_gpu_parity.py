@@ -477,6 +477,18 @@ def test_host_pipeline_rows(kind, fill, cuda_dev):
             got = pipe(hin, hout).numpy().view(np.uint32)
             assert (got == exp).all(), (kind, fill, h, w, cr)
             assert pipe.rows_mode == (cr is not None)
+    # row slabs of one raster with host halo rows (multi-GPU row shards)
+    a = (rng.random((1, 90, 300)) < 0.5).astype(np.uint8)
+    exp = cscan.scan_u8(a, fill)[0]
+    full = torch.from_numpy(a * 7) if kind == "u8" else torch.from_numpy(P.pack_u32(a).view(np.int32))
+    for lo, hi in [(0, 30), (30, 61), (61, 90), (0, 90), (45, 46)]:
+        ha, hb = lo > 0, hi < 90
+        pipe = HostBatchEdges((1, hi - lo, full.shape[2]), kind=kind, width=300, border=fill,
+                              halo_rows=(ha, hb), chunk_rows=7)
+        hin, hout = pipe.new_host_buffers()
+        hin.copy_(full[:, lo - ha:hi + hb])
+        got = pipe(hin, hout).numpy().view(np.uint32)[0]
+        assert (got == exp[lo:hi]).all(), (kind, fill, lo, hi)
     big = synth.c3_words(h=4096)                                     # 4 MiB: automatic rows mode
     pipe = HostBatchEdges((1, 4096, 256), kind="packed", width=8192, border=fill)
     assert pipe.rows_mode
