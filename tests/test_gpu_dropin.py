@@ -86,3 +86,49 @@ def test_device_tensor_input_is_packed_eagerly(cuda_dev):
     assert img._pix is None
     t.zero_()
     assert (img.words == P.from_array(a).words).all()
+
+
+def test_threads_share_the_library(cuda_dev):
+    """The ABI is reentrant (thread-local error text and launch counter, no other
+    state): eight host threads, each on its own stream, mixing kernels, u8/u32
+    inputs and invalid calls, get exact results and their own error messages."""
+    import threading
+
+    import torch
+
+    from oracle import cscan
+    from paper_1401_5245_b200 import cuda as cu
+
+    errors, results = [], {}
+
+    def worker(k):
+        try:
+            rng = np.random.default_rng(100 + k)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for it in range(20):
+                    h, w = int(rng.integers(1, 90)), int(rng.choice([64, 100, 2048, 33]))
+                    a = (rng.random((2, h, w)) < 0.5).astype(np.uint8)
+                    t = torch.from_numpy(a).to(cuda_dev, non_blocking=False)
+                    if it % 2:
+                        got = cu.pack_edges_u8(t, 1)
+                    else:
+                        got = cu.edges_packed(cu.pack_u8(t), w, 1)
+                    try:
+                        cu.edges_packed(cu.pack_u8(t), w + 1000, 1)   # too few words per row
+                    except ValueError as e:
+                        assert "words per row" in str(e)
+                    s.synchronize()
+                    results[(k, it)] = (got.cpu().numpy().view(np.uint32), cscan.scan_u8(a, 1))
+        except Exception as e:      # pragma: no cover - reported below
+            errors.append((k, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t_ in th:
+        t_.start()
+    for t_ in th:
+        t_.join()
+    assert not errors, errors
+    assert len(results) == 160
+    for key, (got, exp) in results.items():
+        assert (got == exp).all(), key
