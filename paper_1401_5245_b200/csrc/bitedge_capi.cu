@@ -246,6 +246,35 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 // Returns 1 when the register-direct kernel does not apply (caller falls back).
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 
+// K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA).
+template <int RSL>
+int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t st) {
+    constexpr int kD = 4;
+    const int64_t nstrips = (rows_total(rp.row_lo, rp.row_hi) + RSL - 1) / RSL;
+    const int64_t nwarps = nstrips * nseg;
+    const unsigned grid = (unsigned)((nwarps + 7) / 8);
+    const size_t smem = (size_t)8 * kD * 2080 + (size_t)8 * kD * 8;
+    rp.nstrips = nstrips;
+#define BE_TMA2(OUTK, H)                                                                        \
+    do {                                                                                        \
+        auto kern = edge_tma2_u8_kernel<RSL, kD, OUTK, H>;                                      \
+        /* per launch: the attribute is per device, and these launches are long */             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
+    } while (0)
+    if (multi) {
+        if (halo) BE_TMA2(kOutAll, true); else BE_TMA2(kOutAll, false);
+    } else if (rp.o_edges && rp.o_eset) {
+        if (halo) BE_TMA2(kOutAny, true); else BE_TMA2(kOutAny, false);
+    } else if (rp.o_eset) {
+        if (halo) BE_TMA2(kOutEset, true); else BE_TMA2(kOutEset, false);
+    } else {
+        if (halo) BE_TMA2(kOutEdges, true); else BE_TMA2(kOutEdges, false);
+    }
+#undef BE_TMA2
+    return cuda_check("edge_tma2_u8_kernel");
+}
+
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
             const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
             uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
@@ -332,34 +361,19 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
     if (input_kind == 1 && G.w >= 2048 && !getenv("BITEDGE_NO_TMA") && !getenv("BITEDGE_TMA1")) {
-        constexpr int kRSLT = 32, kD = 4;
         const int64_t nseg = (G.w + 2047) / 2048;
-        const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
-        const int64_t nwarps = nstrips * nseg;
+        const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
         const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;
-        if ((force || nwarps >= (int64_t)sm_count() * 24) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
-            const unsigned grid = (unsigned)((nwarps + 7) / 8);
-            const size_t smem = (size_t)8 * kD * 2080 + (size_t)8 * kD * 8;
+        if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
+            // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
+            // strips, so the last wave's tail is a quarter as long: C5 737 ->
+            // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
+            // where the 25 % extra staged halo rows of 8-row strips cost more
+            // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
+            const bool short_strips = thr == 1 && !getenv("BITEDGE_TMA2_RSL32");
             const bool halo = above || below;
-            rp.nstrips = nstrips;
-#define BE_TMA2(OUTK, H)                                                                        \
-    do {                                                                                        \
-        auto kern = edge_tma2_u8_kernel<kRSLT, kD, OUTK, H>;                                    \
-        /* per launch: the attribute is per device, and these launches are long */             \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
-    } while (0)
-            if (multi) {
-                if (halo) BE_TMA2(kOutAll, true); else BE_TMA2(kOutAll, false);
-            } else if (rp.o_edges && rp.o_eset) {
-                if (halo) BE_TMA2(kOutAny, true); else BE_TMA2(kOutAny, false);
-            } else if (rp.o_eset) {
-                if (halo) BE_TMA2(kOutEset, true); else BE_TMA2(kOutEset, false);
-            } else {
-                if (halo) BE_TMA2(kOutEdges, true); else BE_TMA2(kOutEdges, false);
-            }
-#undef BE_TMA2
-            return cuda_check("edge_tma2_u8_kernel");
+            return short_strips ? launch_tma2<8>(rp, multi, halo, nseg, st)
+                                : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
     if (multi && input_kind == 1) return 1;          // other uint8 shapes: tile kernel

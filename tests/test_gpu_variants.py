@@ -31,6 +31,7 @@ VARIANTS = {
     "no_tma": {"BITEDGE_NO_TMA": "1"},
     "warpimg_g4": {"BITEDGE_WARPIMG_G4": "1"},
     "pdl_late": {"BITEDGE_PDL_LATE": "1"},
+    "tma_warp_rsl32": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
