@@ -557,22 +557,30 @@ def run_ours(args):
         # one step and its last chunk's kernel + D2H hide behind the next
         # step's H2D (HostBatchEdges.submit does not chain batches)
         pend = [None, None]
-        e0.record()
-        e0.synchronize()                     # every submitted copy starts after e0
-        for i in range(e2e_steps):
-            pend[i & 1] = pipe.submit(hin, houts[i & 1])
-            if i > 0:
-                res = pend[(i - 1) & 1].synchronize()
-                _ = int(res[0, 0, 0])        # step i-1's result, on the host
-        res = pend[(e2e_steps - 1) & 1].synchronize()
-        _ = int(res[0, 0, 0])
-        e1.record()
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
+        # timed in windows; the reported rate is the median window's (robust to
+        # the transient PCIe-rate dips of these boxes, scripts/e2e_windows.py)
+        nwin = 5 if e2e_steps >= 10 else 1
+        per_win = e2e_steps // nwin
+        e2e_steps = per_win * nwin
+        wms = []
+        for _ in range(nwin):
+            e0.record()
+            e0.synchronize()                 # every submitted copy starts after e0
+            for i in range(per_win):
+                pend[i & 1] = pipe.submit(hin, houts[i & 1])
+                if i > 0:
+                    res = pend[(i - 1) & 1].synchronize()
+                    _ = int(res[0, 0, 0])    # step i-1's result, on the host
+            res = pend[(per_win - 1) & 1].synchronize()
+            _ = int(res[0, 0, 0])
+            e1.record()
+            torch.cuda.synchronize()
+            wms.append(e0.elapsed_time(e1))
         if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            t = torch.tensor(wms, device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            wms = [float(v) for v in t.tolist()]
+        ems = statistics.median(wms) * nwin      # median window, as a whole-run time
         px_e2e = px_all
         moved = [int(pipe.h2d_bytes), int(pipe.d2h_bytes)]
         if world > 1:                        # the whole job's bytes per step
@@ -581,7 +589,8 @@ def run_ours(args):
             moved = [int(v) for v in t.tolist()]
         e2e = {"value": px_e2e * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gpixel/s",
                "h2d_bytes_per_step": moved[0], "d2h_bytes_per_step": moved[1],
-               "steps": e2e_steps, "ms_per_step": ems / e2e_steps}
+               "steps": e2e_steps, "ms_per_step": ems / e2e_steps,
+               "windows_gpx_s": [round(px_e2e * per_win / (m / 1e3) / 1e9, 2) for m in wms]}
 
     # ---- parity gate on the measured output (before reporting a number)
     parity = None
