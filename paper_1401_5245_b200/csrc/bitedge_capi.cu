@@ -370,7 +370,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
             // where the 25 % extra staged halo rows of 8-row strips cost more
             // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
-            const bool short_strips = thr == 1 && !getenv("BITEDGE_TMA2_RSL32");
+            const bool short_strips = (thr == 1 || getenv("BITEDGE_TMA2_RSL8")) &&
+                                      !getenv("BITEDGE_TMA2_RSL32");
             const bool halo = above || below;
             return short_strips ? launch_tma2<8>(rp, multi, halo, nseg, st)
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);

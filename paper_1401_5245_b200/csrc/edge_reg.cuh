@@ -272,8 +272,32 @@ edge_reg_packed_kernel(const RegParams p) {
 
 // 32 bytes -> one MSB-first word (pixels x0 .. x0+31); bytes beyond the row are garbage
 // and only ever land in padding bits.
+// General (thresholded) pack of 32 bytes, specialised on t < 128 / t >= 128 so
+// each 4-byte compare is 3 ops (the t-independent form needs a 4-input
+// function): bit 7 of byte k of ge(v) = (byte k >= t).  Two words of flags merge
+// as ga | gb >> 4 (flags at 7,15,23,31 and 3,11,19,27) and one multiply by
+// 2^31+2^22+2^13+2^4 gathers them in pixel order into bits 31..38.
+template <bool HI>
+__device__ __forceinline__ uint32_t ge4(uint32_t v, uint32_t tl) {
+    const uint32_t x = (v | 0x80808080u) - tl;   // bit 7: low 7 bits of the byte >= t & 0x7f
+    return HI ? (v & x & 0x80808080u)             // t >= 128: byte >= 128 and low bits >= tl
+              : ((v | x) & 0x80808080u);          // t < 128: byte >= 128 or low bits >= tl
+}
+
+template <bool HI>
+__device__ __forceinline__ uint32_t pack8_t(uint32_t a, uint32_t b, uint32_t tl) {
+    const uint32_t t = ge4<HI>(a, tl) | (ge4<HI>(b, tl) >> 4);
+    return (uint32_t)(((uint64_t)t * 0x80402010ull) >> 31) & 0xFFu;
+}
+
+template <bool HI>
+__device__ __forceinline__ uint32_t pack32_t(uint4 a, uint4 b, uint32_t tl) {
+    return (pack8_t<HI>(a.x, a.y, tl) << 24) | (pack8_t<HI>(a.z, a.w, tl) << 16) |
+           (pack8_t<HI>(b.x, b.y, tl) << 8) | pack8_t<HI>(b.z, b.w, tl);
+}
+
 __device__ __forceinline__ uint32_t pack32(uint4 a, uint4 b, const Thr &T) {
-    return (pack16(a, T) << 16) | pack16(b, T);
+    return T.m ? pack32_t<false>(a, b, T.tl) : pack32_t<true>(a, b, T.tl);   // launch-uniform
 }
 
 // 8 bytes that are all 0 or 1 -> 8 bits MSB-first: x*16 + y puts the flags of
