@@ -57,7 +57,11 @@ class HostBatchEdges:
             raise ValueError("chunk_rows applies to a single image (n == 1)")
         if self.rows_mode:
             if chunk_rows is None:
-                chunk_rows = max(1, min(8 << 20, per_img // 4) // row_bytes)
+                # two equal chunks up to 128 MiB images, then 64 MiB chunks: per-copy
+                # fixed costs make small chunks slow (scripts/c3_e2e.py: C3 0.22 ms
+                # at 2 x 4 MiB vs 0.27 at 4 x 2 MiB; C4 11.2 ms at 64 MiB chunks vs
+                # 12.6 at 8 MiB)
+                chunk_rows = max(1, min(64 << 20, -(-per_img // 2)) // row_bytes)
             self.chunk = int(chunk_rows)                                    # rows per chunk
             self.d_in = [torch.empty((self.chunk + 2, s), dtype=self.in_dtype, device=self.device)
                          for _ in range(2)]
@@ -65,7 +69,9 @@ class HostBatchEdges:
                                       device=self.device) for _ in range(2)]
         else:
             if chunk_images is None:
-                chunk_images = max(1, min(n, (8 << 20) // max(1, per_img)))  # ~8 MiB per chunk
+                # >= 8 MiB chunks, up to 64 MiB for big batches (fewer, larger copies)
+                target = max(8 << 20, min(64 << 20, n * per_img // 8))
+                chunk_images = max(1, min(n, target // max(1, per_img)))
             self.chunk = int(chunk_images)
             self.d_in = [torch.empty((self.chunk, h, s), dtype=self.in_dtype, device=self.device)
                          for _ in range(2)]
