@@ -100,11 +100,12 @@ bool pdl_enabled() {
 }
 
 template <typename... KArgs, typename... Args>
-void launch_k(void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+void launch_kb(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+               Args... args) {
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(bitedge::kThreads);
+    cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -113,6 +114,11 @@ void launch_k(void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t s
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+    launch_kb(kern, grid, (unsigned)bitedge::kThreads, smem, st, args...);
 }
 
 inline int ilog2(int v) { int l = 0; while ((1 << (l + 1)) <= v) ++l; return l; }
@@ -194,6 +200,7 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cu
         (void)cw;
     } else {
         if (!swap && rs == 2) {
+            // (128-thread CTAs for C3's single wave: +2 % overlapped, -1 % serial; not taken)
             if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
             else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
         } else if (!swap && rs == 8) {

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4:
 edge_reg_packed_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
-    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // 128 or 256 per CTA
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
     const int c = (int)(t - strip * p.items);
