@@ -916,6 +916,7 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     fetch(2, xa, xb, el, er);
     const uint32_t c1a = xa, c1b = xb;
     uint32_t y = y0 + 1 >= p.h ? (y0 + 1) % p.h : y0 + 1;
+#pragma unroll 1   // one copy of the row body: the pack code is large (i-cache)
     for (int k = 3; k < NST - 1; ++k) {               // output rows 1 .. RSL-2
         uint32_t na, nb, nel, ner;
         fetch(k, na, nb, nel, ner);

@@ -44,3 +44,30 @@ def test_hot_kernel_register_budget(frag, budget):
     for name, (regs, st, ld) in hits.items():
         assert regs <= budget, (name, regs, budget)
         assert st == 0 and ld == 0, (name, "spills", st, ld)
+
+
+# SASS size budget (instructions incl. NOPs, `cuobjdump -sass`): K2t2 once grew
+# from 1.8k to 3.7k instructions when a second inlined threshold variant got
+# unrolled into every row of its strip loop, and C5 lost 47 % to instruction-
+# cache misses (676 -> 994 us) with no change in registers.
+SASS_BUDGET = {
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0EEEvNS_9RegParamsE": 950,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0EEEvNS_9RegParamsE": 1450,
+    "_ZN7bitedge20edge_warp_img_kernelILi1ELi0ELi8EEEvNS_9RegParamsEil": 1550,
+    "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0EEEvNS_9RegParamsEll": 2800,
+}
+
+
+@pytest.mark.parametrize("fn,budget", sorted(SASS_BUDGET.items()))
+def test_hot_kernel_code_size(fn, budget):
+    import shutil
+    import subprocess
+
+    so = os.path.join(os.path.dirname(LOG), "libbitedge_cuda.so")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(so) or not os.path.exists(tool):
+        pytest.skip("library or cuobjdump missing")
+    out = subprocess.run([tool, "-sass", "-fun", fn, so], capture_output=True, text=True).stdout
+    n = len(re.findall(r"^\s+/\*[0-9a-f]{4}\*/", out, flags=re.M))
+    assert n > 0, f"{fn} not found"
+    assert n <= budget, (fn, n, budget)
