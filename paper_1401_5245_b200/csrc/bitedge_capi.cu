@@ -299,6 +299,12 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     for (int k = 0; k < 4; ++k) rp.o_side[k] = o_side[k];
     rp.o_packed = o_packed;
     const bool multi = multi_out(rp);
+    // uint8 -> uint64 words (the drop-in BitImage layout): only K2t2 stores
+    // swapped halves; it takes every such shape >= 1024 px wide, the tile kernel
+    // the rest
+    const bool u64_out = input_kind == 1 && G.swap;
+    if (u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"))) return 1;
+    rp.oswap = u64_out ? 1 : 0;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
@@ -321,7 +327,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
     for (int k = 0; k < 4; ++k) rp.vst = rp.vst && al(o_side[k], 4 * ocw);
     rp.vst = rp.vst && al(o_packed, 4 * ocw);
-    if (input_kind == 1 && !multi && !above && !below && row_lo == 0 && row_hi == nrows &&
+    if (input_kind == 1 && !multi && !u64_out && !above && !below && row_lo == 0 && row_hi == nrows &&
         in_row_bytes == G.w && ((uintptr_t)in % 32) == 0 && G.w % 32 == 0 && G.wp <= 32 &&
         (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !getenv("BITEDGE_NO_WARPIMG")) {
         const int lwpr = ilog2(G.wp), rpi = 32 >> lwpr;
@@ -367,10 +373,11 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
-    if (input_kind == 1 && G.w >= 2048 && !getenv("BITEDGE_NO_TMA") && !getenv("BITEDGE_TMA1")) {
+    if (input_kind == 1 && (G.w >= 2048 || u64_out) && !getenv("BITEDGE_NO_TMA") &&
+        (!getenv("BITEDGE_TMA1") || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
-        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr || u64_out;
         if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
             // strips, so the last wave's tail is a quarter as long: C5 737 ->
@@ -384,7 +391,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
-    if (multi && input_kind == 1) return 1;          // other uint8 shapes: tile kernel
+    if ((multi || u64_out) && input_kind == 1) return 1;   // other uint8 shapes: tile kernel
     if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
@@ -596,11 +603,9 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     if (in_stride < w) return fail(BE_EINVAL, "input row stride %lld bytes < width %lld",
                                    (long long)in_stride, (long long)w);
     tp.in_stride = in_stride;
-    if (word_bits == 32) {
-        rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, o_side, o_packed,
-                     tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
-        if (rc != 1) return rc;
-    }
+    rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, o_side, o_packed,
+                 tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
+    if (rc != 1) return rc;
     if (only_edges && word_bits == 32) {
         rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
                         G, nrows, row_lo, row_hi, st, thr);

@@ -50,6 +50,7 @@ struct RegParams {
     uint32_t *o_side[4];     // kOutAll only: fundamental edges L, R, U, D (or nullptr)
     uint32_t *o_packed;      // kOutAll only: the packed input, padding 1 (or nullptr)
     int pdl_late;            // K2w: signal dependents after the stores, not at entry
+    int oswap;               // K2t2: 1 = uint64 output words (pixel word p at uint32 index p ^ 1)
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -764,7 +765,7 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
 // integer offsets from one base pointer; only the first/last staged rows can be
 // absent or come from the halo buffers.
 template <int RSL, int D, int OUT, bool HALO>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)   // smem allows 3 CTAs/SM: up to 80 regs, no spills
 edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     const Thr T = make_thr(p.thr);
     constexpr int SEG = 2048;                        // pixels (bytes) per warp segment
@@ -788,6 +789,9 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     const int64_t g0 = p.row_lo + strip * RSL;
     const int64_t x0 = (int64_t)seg * SEG;
     const int ca = seg * 64 + lane, cb = ca + 32;    // this lane's two output words
+    // their uint32 store columns: uint64 output stores pixel word c at c ^ 1
+    // (the row stride is then even, so the swap stays inside the row)
+    const int cas = ca ^ p.oswap, cbs = cb ^ p.oswap;
     const uint32_t fw = p.fillword;
     const int64_t rb = p.in_row_bytes;
     const int64_t wr = (p.w + 15) & ~(int64_t)15;
@@ -866,7 +870,8 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
         const uint32_t lwb = lane == 0 ? a31 : b_up;
         const uint32_t rwb = lane == 31 ? er : b_dn;
         if (g0 + r < p.row_hi) {
-            const int64_t o = (g0 + r) * p.out_stride + ca;
+            const int64_t orow = (g0 + r) * p.out_stride;
+            const int64_t oa = orow + cas, ob = orow + cbs;
             const bool top = y == 0 && !(HALO && p.above);
             const bool bot = y == p.h - 1 && !(HALO && p.below);
             const uint32_t uA = top ? fw : ua, uB = top ? fw : ub;
@@ -887,17 +892,17 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
 #pragma unroll
                 for (int k = 0; k < 7; ++k) {
                     if (dst[k] == nullptr) continue;
-                    if (la) __stcs(dst[k] + o, va[k]);
-                    if (lb_) __stcs(dst[k] + o + 32, vb[k]);
+                    if (la) __stcs(dst[k] + oa, va[k]);
+                    if (lb_) __stcs(dst[k] + ob, vb[k]);
                 }
             } else {
                 if (la) {
-                    if (OUT != kOutEset) __stcs(p.o_edges + o, xa | ~anyA | ga);
-                    if (OUT != kOutEdges) __stcs(p.o_eset + o, (~xa & anyA) | ga);
+                    if (OUT != kOutEset) __stcs(p.o_edges + oa, xa | ~anyA | ga);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + oa, (~xa & anyA) | ga);
                 }
                 if (lb_) {
-                    if (OUT != kOutEset) __stcs(p.o_edges + o + 32, xb | ~anyB | gb);
-                    if (OUT != kOutEdges) __stcs(p.o_eset + o + 32, (~xb & anyB) | gb);
+                    if (OUT != kOutEset) __stcs(p.o_edges + ob, xb | ~anyB | gb);
+                    if (OUT != kOutEdges) __stcs(p.o_eset + ob, (~xb & anyB) | gb);
                 }
             }
         }

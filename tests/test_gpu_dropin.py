@@ -132,3 +132,38 @@ def test_threads_share_the_library(cuda_dev):
     assert len(results) == 160
     for key, (got, exp) in results.items():
         assert (got == exp).all(), key
+
+
+@pytest.mark.parametrize("w", [1024, 1056, 1100, 2048, 2080, 3000, 4096, 100])
+def test_u8_to_u64_words(w, cuda_dev):
+    """uint8 pixels -> uint64 words (the BitImage layout) through K2t2's swapped
+    stores (w >= 1024) or the tile kernel: pack, fused pack+edges, every output,
+    BLACK_OUTSIDE, a threshold; padding words included (odd uint32 counts)."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(w)
+    for n, h in [(1, 37), (3, 9)]:
+        a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
+        g = torch.from_numpy(a * rng.integers(1, 256, a.shape).astype(np.uint8)).to(cuda_dev)
+        refs = [P.from_array(x) for x in a]
+        pk = cu.pack_u8(g, word_bits=64).cpu().numpy().view(np.uint64)
+        assert (pk == np.stack([r.words for r in refs])).all(), (w, n, h)
+        for fill in (1, 0):
+            e, p2 = cu.pack_and_edges(g, fill, word_bits=64)
+            exp = np.stack([P.detect_edges_mask(r, fill).words for r in refs])
+            assert (e.cpu().numpy().view(np.uint64) == exp).all(), (w, n, h, fill)
+            assert (p2.cpu().numpy().view(np.uint64) == np.stack([r.words for r in refs])).all()
+        res = cu.edges_general(g, None, 1, word_bits=64, edgeset=True, sides=True, packed=True)
+        for k, d in (("left", P.LEFT), ("right", P.RIGHT), ("up", P.UP), ("down", P.DOWN)):
+            exp = np.stack([P.fundamental_edge(r, P.build_mask(r), d, 1).words for r in refs])
+            assert (res[k].cpu().numpy().view(np.uint64) == exp).all(), (w, k)
+        exp = np.stack([P.edge_set(r, 1).words for r in refs])
+        assert (res["edgeset"].cpu().numpy().view(np.uint64) == exp).all()
+        # a threshold: gray >= 200 is white
+        gray = torch.from_numpy(rng.integers(0, 256, (n, h, w)).astype(np.uint8)).to(cuda_dev)
+        th = cu.threshold_u8(gray, 200, word_bits=64).cpu().numpy().view(np.uint64)
+        expt = np.stack([P.from_array((x >= 200).astype(np.uint8)).words
+                         for x in gray.cpu().numpy()])
+        assert (th == expt).all(), (w, "threshold")

@@ -18,7 +18,7 @@ BUDGET = {
     "edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0E": 64,   # C3: K1 2-row, 8-word items
     "edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0E": 80,   # C4: K1 4-row, 8-word items
     "edge_warp_img_kernelILi1ELi0ELi8E": 80,                 # C2: K2w, 64-px rows
-    "edge_tma2_u8_kernelILi8ELi4ELi0ELb0E": 64,             # C5: K2t2
+    "edge_tma2_u8_kernelILi8ELi4ELi0ELb0E": 80,             # C5: K2t2 (smem caps it at 3 CTAs/SM)
     "edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb1E": 80,   # F1: P4 4-row
     "edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb1E": 64,   # F1: P4 2-row
 }
