@@ -1,3 +1,3 @@
 """`bitedge.binarize` (reference: SPEC.md:226-271, module not shipped) -> B200
-implementation of the fixed threshold (Otsu is out of scope)."""
-from paper_1401_5245_b200.binarize import threshold, threshold_edges  # noqa: F401
+implementation: fixed threshold, fused threshold + edges, Otsu."""
+from paper_1401_5245_b200.binarize import otsu_threshold, threshold, threshold_edges  # noqa: F401

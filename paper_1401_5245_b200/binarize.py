@@ -1,10 +1,11 @@
-"""`bitedge.binarize.threshold` on the device (the reference
-ships no binarize module).  Only the fixed-threshold rule is provided -- it is
-the piece SURVEY 8(f) F2 fuses into the edge kernels; Otsu is
-out of scope.
+"""`bitedge.binarize` on the device (the reference ships no
+binarize module).  The fixed-threshold rule is the piece SURVEY 8(f) F2 fuses
+into the edge kernels; Otsu picks the threshold from a device
+histogram.
 
     threshold(gray, t) -> BitImage      pixel -> White iff sample >= t
     threshold_edges(gray, t, border)    (binarised, edges); batches: cuda.threshold_edges_u8
+    otsu_threshold(gray) -> int         between-class-variance maximiser, ties -> smaller t
 """
 
 from __future__ import annotations
@@ -50,3 +51,24 @@ def threshold_edges(gray, t: int, border: BorderPolicy = BorderPolicy.WHITE_OUTS
 
     binary = threshold(gray, t)
     return binary, detect_edges_mask(binary, border)
+
+
+def otsu_threshold(gray: np.ndarray) -> int:
+    """Between-class-variance maximiser over the 256-bin histogram; ties go to the
+    smaller threshold.  Histogram on the device."""
+    torch = _torch()
+    g = _gray_tensor(gray).reshape(-1)
+    hist = torch.bincount(g.to(torch.int64), minlength=256).to(torch.float64)
+    total = hist.sum()
+    t = torch.arange(256, dtype=torch.float64, device=g.device)
+    w0 = torch.cumsum(hist, 0) - hist             # samples < t  (black class for threshold t)
+    m0 = torch.cumsum(hist * t, 0) - hist * t
+    w1 = total - w0
+    m1 = (hist * t).sum() - m0
+    valid = (w0 > 0) & (w1 > 0)
+    var = torch.where(valid, w0 * w1 * (m0 / w0.clamp(min=1) - m1 / w1.clamp(min=1)) ** 2,
+                      torch.zeros_like(w0))
+    best = var.max()
+    if best <= 0:
+        return 0
+    return int(torch.nonzero(var >= best * (1 - 1e-12))[0].item())

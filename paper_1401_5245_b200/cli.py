@@ -29,6 +29,9 @@ class CliError(Exception):
     """Usage / I/O problem -> exit code 2."""
 
 
+from .binarize import otsu_threshold  # noqa: E402,F401  (re-exported for the CLI)
+
+
 def _read(path: str) -> bytes:
     try:
         with open(path, "rb") as f:
@@ -106,30 +109,6 @@ def read_pgm(data: bytes):
     if len(toks) < w * h:
         raise ValueError(f"short PGM payload: need {w * h} samples after offset {pos}")
     return np.array([int(t) for t in toks[: w * h]], np.uint8).reshape(h, w)
-
-
-def otsu_threshold(gray: np.ndarray) -> int:
-    """Between-class-variance maximiser over the 256-bin histogram; ties go to the
-    smaller threshold.  Histogram on the device."""
-    import torch
-
-    from .bitimage import _device
-
-    g = torch.from_numpy(np.ascontiguousarray(gray).reshape(-1)).to(_device())
-    hist = torch.bincount(g.to(torch.int64), minlength=256).to(torch.float64)
-    total = hist.sum()
-    t = torch.arange(256, dtype=torch.float64, device=g.device)
-    w0 = torch.cumsum(hist, 0) - hist             # samples < t  (black class for threshold t)
-    m0 = torch.cumsum(hist * t, 0) - hist * t
-    w1 = total - w0
-    m1 = (hist * t).sum() - m0
-    valid = (w0 > 0) & (w1 > 0)
-    var = torch.where(valid, w0 * w1 * (m0 / w0.clamp(min=1) - m1 / w1.clamp(min=1)) ** 2,
-                      torch.zeros_like(w0))
-    best = var.max()
-    if best <= 0:
-        return 0
-    return int(torch.nonzero(var >= best * (1 - 1e-12))[0].item())
 
 
 # ---------------------------------------------------------------- bench shapes
