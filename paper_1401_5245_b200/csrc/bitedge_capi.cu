@@ -339,14 +339,14 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
 #define BE_WARPIMG_G(L, GM)                                                                    \
     do {                                                                                       \
         if (o_edges && o_eset)                                                                 \
-            launch_k(edge_warp_img_kernel<L, kOutAny, GM>, (unsigned)grid, 0, st, rp, groups,  \
-                     nimg);                                                                    \
+            launch_kb(edge_warp_img_kernel<L, kOutAny, GM>, wgrid, wblock, wsmem, st, rp,      \
+                      groups, nimg);                                                           \
         else if (o_eset)                                                                       \
-            launch_k(edge_warp_img_kernel<L, kOutEset, GM>, (unsigned)grid, 0, st, rp, groups, \
-                     nimg);                                                                    \
+            launch_kb(edge_warp_img_kernel<L, kOutEset, GM>, wgrid, wblock, wsmem, st, rp,     \
+                      groups, nimg);                                                           \
         else                                                                                   \
-            launch_k(edge_warp_img_kernel<L, kOutEdges, GM>, (unsigned)grid, 0, st, rp,        \
-                     groups, nimg);                                                            \
+            launch_kb(edge_warp_img_kernel<L, kOutEdges, GM>, wgrid, wblock, wsmem, st, rp,    \
+                      groups, nimg);                                                           \
     } while (0)
 #define BE_WARPIMG(L)                                                                          \
     case L:                                                                                    \
@@ -356,6 +356,12 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                 // overlapped batches but 9 % slower serially under PDL than GMAX = 8
                 // (77 regs, 1.15 waves): opt-in knob.
                 const bool g8 = getenv("BITEDGE_WARPIMG_G4") == nullptr;
+                // (Capping residency at one wave with 128-thread CTAs + 32 KB of
+                // dummy smem -- 28 warps/SM, 4144 slots for 4096 images -- was
+                // 20 % slower overlapped and serially: not taken.)
+                const unsigned wblock = (unsigned)kThreads;
+                const unsigned wgrid = (unsigned)grid;
+                const size_t wsmem = 0;
                 rp.pdl_late = getenv("BITEDGE_PDL_LATE") != nullptr;
                 switch (lwpr) {
                     BE_WARPIMG(0)

@@ -360,7 +360,7 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
     const Thr T = make_thr(p.thr);
     constexpr int WPR = 1 << LWPR;
     constexpr int RPI = 32 >> LWPR;
-    const int64_t img = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int64_t img = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (img >= nimg) return;                      // whole warps exit together
     const int lane = threadIdx.x & 31;
     const int rl = lane >> LWPR, wi = lane & (WPR - 1);
