@@ -91,7 +91,10 @@ int be_pack_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int6
 /* K3. K1 on a row slab of one image whose row -1 / row `rows` come from
  * neighbour slabs (the received halo rows) instead of the border fill; only
  * output rows [row_lo, row_hi) are written.  A NULL halo means the slab touches
- * the image border there and the fill applies (bitimage.py:216-223). */
+ * the image border there and the fill applies (bitimage.py:216-223).
+ * `row_stride_words` (the slab's and the output's stride, >= ceil(w/32)) is
+ * one argument more than SURVEY.md 8(b) sketched: slabs cut from a padded
+ * raster keep its stride. */
 int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
                             const uint32_t *below_or_null, uint32_t *out, int64_t rows, int64_t w,
                             int64_t row_stride_words, int fill_bit, int64_t row_lo, int64_t row_hi,
@@ -160,8 +163,9 @@ int be_p4_encode(const void *in, uint8_t *p4, int word_bits, int64_t n, int64_t 
                  int64_t in_row_stride_words, void *stream);
 /* detect_edges_mask from a P4 payload to a P4 payload.  When a P4 row is a whole
  * number of 16-byte chunks (w % 128 in 121..128 or 0) kernel K1 reads and writes
- * P4 directly (byte swap + inversion in registers, 0.25 B/px); otherwise it runs
- * decode -> K1 -> encode through `scratch_or_null` (2 * n * h * ceil(w/32) words). */
+ * P4 directly (kept in the P4 byte order; only the centre row is byte-swapped for
+ * the horizontal shifts, 0.25 B/px); otherwise it runs decode -> K1 -> encode
+ * through `scratch_or_null` (2 * n * h * ceil(w/32) words). */
 int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int64_t h, int64_t w,
                 int fill_bit, uint32_t *scratch_or_null, void *stream);
 
