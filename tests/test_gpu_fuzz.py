@@ -119,7 +119,7 @@ def test_fuzz_halo_slabs_all_inputs(knob, cuda_dev, monkeypatch):
             "u8": (torch.from_numpy(a).to(cuda_dev), 32),
             "u8_to_u64": (torch.from_numpy(a).to(cuda_dev), 64),
             "u32": (torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev), 32),
-            "u64": (torch.from_numpy(P.from_array(a).words.view(np.int64)).to(cuda_dev), 64),
+            "u64": (torch.from_numpy(P.from_array(a).words.view(np.int64).copy()).to(cuda_dev), 64),
         }
         img = P.from_array(a)
         mask = P.build_mask(img)
