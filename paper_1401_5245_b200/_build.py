@@ -12,15 +12,13 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbitedge_cuda.so")
-SOURCES = ["bitedge_capi.cu"]
-HEADERS = ["edge_tile.cuh", "edge_stream.cuh", "edge_reg.cuh", os.path.join("..", "..", "include", "bitedge.h")]
+# one translation unit per concern, compiled in parallel then linked
+SOURCES = ["capi_edges.cu", "capi_words.cu", "capi_p4.cu", "capi_host.cu"]
+HEADERS = ["capi_internal.cuh", "edge_tile.cuh", "edge_stream.cuh", "edge_reg.cuh",
+           os.path.join("..", "..", "include", "bitedge.h")]
 
-NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-lineinfo",
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-v",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc() -> str:
@@ -41,18 +39,37 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB_PATH
+    import concurrent.futures as cf
+    import tempfile
+
     os.makedirs(LIB_DIR, exist_ok=True)
-    srcs = [os.path.join(CSRC, f) for f in SOURCES]
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *srcs]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    tmpdir = tempfile.mkdtemp(prefix="bitedge_build_")
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def compile_one(src):
+        obj = os.path.join(tmpdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *inc, "-c", "-o", obj, os.path.join(CSRC, src)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        return obj, res.stderr
+
+    try:
+        with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        tmp = LIB_PATH + ".tmp"
+        cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *[o for o, _ in results]]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc link failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        os.replace(tmp, LIB_PATH)
+    finally:
+        shutil.rmtree(tmpdir, ignore_errors=True)
+    log = "".join(err for _, err in results)
     if verbose:
-        print(res.stderr)
-    os.replace(tmp, LIB_PATH)
+        print(log)
     with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
-        f.write(res.stderr)
+        f.write(log)
     return LIB_PATH
 
 

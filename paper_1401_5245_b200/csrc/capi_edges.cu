@@ -1,0 +1,583 @@
+// capi_edges.cu -- the fused edge kernels' host side: kernel selection (tile /
+// TMA-stream / register-direct K1, K2, K2w, K2r, K2t, K2t2, halos, multi-output)
+// and the C-ABI entry points that compute edges (include/bitedge.h).
+#include "capi_internal.cuh"
+#include "edge_reg.cuh"
+#include "edge_stream.cuh"
+
+using namespace bitedge;
+using namespace bitedge::capi;
+
+namespace bitedge {
+namespace capi {
+
+template <int KIND>
+int launch_tile(TileParams &tp, int64_t rows, cudaStream_t st) {
+    const int TQ = 1 << tp.log_tq, R = 1 << tp.log_r;
+    const size_t smem = (size_t)(R + 2) * (TQ + 8) * 4 + R;
+    const int64_t tiles_y = (rows + R - 1) / R;
+    const int64_t grid = tiles_y * tp.tiles_x;
+    if (grid <= 0) return BE_OK;
+    if (grid > 0x7FFFFFFFLL) return fail(BE_EINVAL, "raster too large for one launch");
+    const bool others = tp.o_side[0] || tp.o_side[1] || tp.o_side[2] || tp.o_side[3] || tp.o_packed;
+    if (!others && tp.o_edges && !tp.o_eset)
+        edge_tile_kernel<KIND, kOutEdges><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    else if (!others && tp.o_eset && !tp.o_edges)
+        edge_tile_kernel<KIND, kOutEset><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    else
+        edge_tile_kernel<KIND, kOutAny><<<(unsigned)grid, kThreads, smem, st>>>(tp);
+    return cuda_check("edge_tile_kernel");
+}
+
+// ---------------------------------------------------------------- streaming kernel
+
+// Kernel selection knob for A/B measurements: BITEDGE_KERNEL=tile forces the
+// one-shot tile kernel, =stream forbids nothing (default: stream when eligible).
+bool stream_allowed() {
+    const char *e = getenv("BITEDGE_KERNEL");
+    return !(e && strcmp(e, "tile") == 0);
+}
+
+template <int KIND, int OUT>
+int launch_stream_out(StreamParams &sp, size_t smem, cudaStream_t st) {
+    if (smem > 48 * 1024) {   // per launch: the attribute is per device
+        cudaError_t e = cudaFuncSetAttribute(edge_stream_kernel<KIND, OUT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail((int)e, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_stream_kernel<KIND, OUT>, kThreads,
+                                                  smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > sp.ntiles) grid = sp.ntiles;
+    edge_stream_kernel<KIND, OUT><<<(unsigned)grid, kThreads, smem, st>>>(sp);
+    return cuda_check("edge_stream_kernel");
+}
+
+template <int KIND>
+int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
+    if (sp.o_edges && sp.o_eset) return launch_stream_out<KIND, kOutAny>(sp, smem, st);
+    if (sp.o_eset) return launch_stream_out<KIND, kOutEset>(sp, smem, st);
+    return launch_stream_out<KIND, kOutEdges>(sp, smem, st);
+}
+
+// ---------------------------------------------------------------- register-direct kernel
+
+// Launch helpers: dispatch the runtime choices onto template parameters.
+template <int OUT, bool HALO>
+int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
+    if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
+        if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
+        else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        (void)cw;
+    } else {
+        if (!swap && rs == 2) {
+            // (128-thread CTAs for C3's single wave: +2 % overlapped, -1 % serial; not taken)
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
+        } else if (!swap && rs == 8) {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp);
+        } else if (swap) {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        } else {
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp);
+            else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        }
+    }
+    return cuda_check("edge_reg_packed_kernel");
+}
+
+template <int OUT, bool HALO>
+int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
+    if (rp.v8) {
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, 0, st, rp);
+    } else {
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, 0, st, rp);
+    }
+    return cuda_check("edge_reg_u8_kernel");
+}
+
+inline bool multi_out(const RegParams &rp) {
+    return rp.o_side[0] || rp.o_side[1] || rp.o_side[2] || rp.o_side[3] || rp.o_packed;
+}
+
+template <bool HALO>
+int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
+                    cudaStream_t st) {
+    if (multi_out(rp)) {          // packed input only (uint8 multi-output goes to K2t2 or tile)
+        if (input_kind == 1) return 1;
+        return launch_reg_packed<kOutAll, HALO>(rp, swap, cw, rs, grid, st);
+    }
+    if (input_kind == 1) {
+        if (rp.o_edges && rp.o_eset) return launch_reg_u8<kOutAny, HALO>(rp, rs, grid, st);
+        if (rp.o_eset) return launch_reg_u8<kOutEset, HALO>(rp, rs, grid, st);
+        return launch_reg_u8<kOutEdges, HALO>(rp, rs, grid, st);
+    }
+    if (rp.o_edges && rp.o_eset) return launch_reg_packed<kOutAny, HALO>(rp, swap, cw, rs, grid, st);
+    if (rp.o_eset) return launch_reg_packed<kOutEset, HALO>(rp, swap, cw, rs, grid, st);
+    return launch_reg_packed<kOutEdges, HALO>(rp, swap, cw, rs, grid, st);
+}
+
+// Returns 1 when the register-direct kernel does not apply (caller falls back).
+inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
+
+// K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA).
+template <int RSL>
+int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t st) {
+    constexpr int kD = 4;
+    const int64_t nstrips = (rows_total(rp.row_lo, rp.row_hi) + RSL - 1) / RSL;
+    const int64_t nwarps = nstrips * nseg;
+    const unsigned grid = (unsigned)((nwarps + 7) / 8);
+    const size_t smem = (size_t)8 * kD * 2080 + (size_t)8 * kD * 8;
+    rp.nstrips = nstrips;
+#define BE_TMA2(OUTK, H)                                                                        \
+    do {                                                                                        \
+        auto kern = edge_tma2_u8_kernel<RSL, kD, OUTK, H>;                                      \
+        /* per launch: the attribute is per device, and these launches are long */             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
+    } while (0)
+    if (multi) {
+        if (halo) BE_TMA2(kOutAll, true); else BE_TMA2(kOutAll, false);
+    } else if (rp.o_edges && rp.o_eset) {
+        if (halo) BE_TMA2(kOutAny, true); else BE_TMA2(kOutAny, false);
+    } else if (rp.o_eset) {
+        if (halo) BE_TMA2(kOutEset, true); else BE_TMA2(kOutEset, false);
+    } else {
+        if (halo) BE_TMA2(kOutEdges, true); else BE_TMA2(kOutEdges, false);
+    }
+#undef BE_TMA2
+    return cuda_check("edge_tma2_u8_kernel");
+}
+
+int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
+            const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
+            uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
+            int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
+    const char *e = getenv("BITEDGE_KERNEL");
+    if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return 1;
+    auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
+    if (G.h >= ((int64_t)1 << 31)) return 1;
+    RegParams rp;
+    memset(&rp, 0, sizeof(rp));
+    rp.in = (const char *)in; rp.above = (const char *)above; rp.below = (const char *)below;
+    rp.in_row_bytes = in_row_bytes;
+    rp.o_edges = o_edges; rp.o_eset = o_eset; rp.out_stride = out_stride_u32;
+    for (int k = 0; k < 4; ++k) rp.o_side[k] = o_side[k];
+    rp.o_packed = o_packed;
+    const bool multi = multi_out(rp);
+    // uint8 -> uint64 words (the drop-in BitImage layout): only K2t2 stores
+    // swapped halves; it takes every such shape >= 1024 px wide, the tile kernel
+    // the rest
+    const bool u64_out = input_kind == 1 && G.swap;
+    if (u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"))) return 1;
+    rp.oswap = u64_out ? 1 : 0;
+    rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
+    rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
+    rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
+    auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+    const bool in32 = al(in, 32) && in_row_bytes % 32 == 0 && al(above, 32) && al(below, 32);
+    // packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4
+    // Packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4.
+    // Small rasters (< 4 waves of 4-row strips) use 2-row strips instead, which
+    // doubles the threads in flight (C3: 5.1 us serial / 88 % overlapped vs
+    // 5.3 / 79 % for 4-word x 4-row items; scripts/c3sweep.sh).
+    const int64_t strips4 = (row_hi - row_lo + 3) / 4;
+    const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
+    int cw = (input_kind == 0 && in32 && !multi && !getenv("BITEDGE_CW4")) ? 8 : 4;
+    const int packed_rs = (input_kind == 0 && !G.swap && !big) ? 2 : 4;
+    if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
+    rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
+    rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
+    rp.thr = thr;
+    const int ocw = input_kind == 1 ? 1 : cw;
+    rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
+    for (int k = 0; k < 4; ++k) rp.vst = rp.vst && al(o_side[k], 4 * ocw);
+    rp.vst = rp.vst && al(o_packed, 4 * ocw);
+    if (input_kind == 1 && !multi && !u64_out && !above && !below && row_lo == 0 && row_hi == nrows &&
+        in_row_bytes == G.w && ((uintptr_t)in % 32) == 0 && G.w % 32 == 0 && G.wp <= 32 &&
+        (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !getenv("BITEDGE_NO_WARPIMG")) {
+        const int lwpr = ilog2(G.wp), rpi = 32 >> lwpr;
+        if (G.h % rpi == 0 && G.h / rpi <= 8) {
+            const int groups = (int)(G.h / rpi);
+            const int64_t nimg = G.n;
+            const int64_t grid = (nimg * 32 + kThreads - 1) / kThreads;
+            if (grid <= 0x7FFFFFFFLL) {
+#define BE_WARPIMG_G(L, GM)                                                                    \
+    do {                                                                                       \
+        if (o_edges && o_eset)                                                                 \
+            launch_kb(edge_warp_img_kernel<L, kOutAny, GM>, wgrid, wblock, wsmem, st, rp,      \
+                      groups, nimg);                                                           \
+        else if (o_eset)                                                                       \
+            launch_kb(edge_warp_img_kernel<L, kOutEset, GM>, wgrid, wblock, wsmem, st, rp,     \
+                      groups, nimg);                                                           \
+        else                                                                                   \
+            launch_kb(edge_warp_img_kernel<L, kOutEdges, GM>, wgrid, wblock, wsmem, st, rp,    \
+                      groups, nimg);                                                           \
+    } while (0)
+#define BE_WARPIMG(L)                                                                          \
+    case L:                                                                                    \
+        if (groups <= 4 && !g8) BE_WARPIMG_G(L, 4); else BE_WARPIMG_G(L, 8);                   \
+        return cuda_check("edge_warp_img_kernel");
+                // GMAX = 4 (48 regs, one wave of 4096 C2 images) is 1.5 % faster with
+                // overlapped batches but 9 % slower serially under PDL than GMAX = 8
+                // (77 regs, 1.15 waves): opt-in knob.
+                const bool g8 = getenv("BITEDGE_WARPIMG_G4") == nullptr;
+                // (Capping residency at one wave with 128-thread CTAs + 32 KB of
+                // dummy smem -- 28 warps/SM, 4144 slots for 4096 images -- was
+                // 20 % slower overlapped and serially: not taken.)
+                const unsigned wblock = (unsigned)kThreads;
+                const unsigned wgrid = (unsigned)grid;
+                const size_t wsmem = 0;
+                rp.pdl_late = getenv("BITEDGE_PDL_LATE") != nullptr;
+                switch (lwpr) {
+                    BE_WARPIMG(0)
+                    BE_WARPIMG(1)
+                    BE_WARPIMG(2)
+                    BE_WARPIMG(3)
+                    BE_WARPIMG(4)
+                    BE_WARPIMG(5)
+                    default: break;
+                }
+#undef BE_WARPIMG
+#undef BE_WARPIMG_G
+            }
+        }
+    }
+    const int64_t rows = row_hi - row_lo;
+    // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
+    if (input_kind == 1 && (G.w >= 2048 || u64_out) && !getenv("BITEDGE_NO_TMA") &&
+        (!getenv("BITEDGE_TMA1") || u64_out)) {
+        const int64_t nseg = (G.w + 2047) / 2048;
+        const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr || u64_out;
+        if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
+            // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
+            // strips, so the last wave's tail is a quarter as long: C5 737 ->
+            // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
+            // where the 25 % extra staged halo rows of 8-row strips cost more
+            // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
+            const bool short_strips = (thr == 1 || getenv("BITEDGE_TMA2_RSL8")) &&
+                                      !getenv("BITEDGE_TMA2_RSL32");
+            const bool halo = above || below;
+            return short_strips ? launch_tma2<8>(rp, multi, halo, nseg, st)
+                                : launch_tma2<32>(rp, multi, halo, nseg, st);
+        }
+    }
+    if ((multi || u64_out) && input_kind == 1) return 1;   // other uint8 shapes: tile kernel
+    if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
+        constexpr int kRSLT = 32, kD = 6;
+        const int64_t nseg = (G.w + 1023) / 1024;
+        const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
+        const int64_t nwarps = nstrips * nseg;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;   // tests: any size
+        if ((force || nwarps >= (int64_t)sm_count() * 32) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
+            const unsigned grid = (unsigned)((nwarps + 7) / 8);
+            const size_t smem = (size_t)8 * kD * 1056 + (size_t)8 * kD * 8;
+            const bool halo = above || below;
+            rp.nstrips = nstrips;
+#define BE_TMA(OUTK, H)                                                                         \
+    do {                                                                                        \
+        auto kern = edge_tma_u8_kernel<kRSLT, kD, OUTK, H>;                                     \
+        /* per launch: the attribute is per device, and these launches are long */             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
+    } while (0)
+            if (rp.o_edges && rp.o_eset) {
+                if (halo) BE_TMA(kOutAny, true); else BE_TMA(kOutAny, false);
+            } else if (rp.o_eset) {
+                if (halo) BE_TMA(kOutEset, true); else BE_TMA(kOutEset, false);
+            } else {
+                if (halo) BE_TMA(kOutEdges, true); else BE_TMA(kOutEdges, false);
+            }
+#undef BE_TMA
+            return cuda_check("edge_tma_u8_kernel");
+        }
+    }
+    // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
+    constexpr int kRSL = 32, kQ = 4;
+    if (input_kind == 1 && rp.v8 && !getenv("BITEDGE_NO_ROLL") &&
+        (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
+        rp.nstrips = (rows + kRSL - 1) / kRSL;
+        const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
+        if (g <= 0x7FFFFFFFLL) {
+            const unsigned grid = (unsigned)g;
+            const bool halo = above || below;
+            if (rp.o_edges && rp.o_eset) {
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutAny, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutAny, false>, grid, 0, st, rp);
+            } else if (rp.o_eset) {
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEset, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEset, false>, grid, 0, st, rp);
+            } else {
+                if (halo) launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEdges, true>, grid, 0, st, rp);
+                else launch_k(edge_roll_u8_kernel<kRSL, kQ, kOutEdges, false>, grid, 0, st, rp);
+            }
+            return cuda_check("edge_roll_u8_kernel");
+        }
+    }
+    // strip height: 4 rows (the one-shot kernels keep every row of the strip in flight)
+    int rs = input_kind == 0 ? packed_rs : 4;
+    if (input_kind == 1) {
+        const char *rse = getenv("BITEDGE_RS");
+        if (rse) rs = atoi(rse) == 8 ? 8 : 4;
+    } else if (!G.swap) {
+        const char *rse = getenv("BITEDGE_PRS");      // packed strip height experiments: 2/4/8
+        if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
+    }
+    if (multi && rs == 8) rs = 4;                    // kOutAll has 2- and 4-row strips
+    rp.nstrips = (rows + rs - 1) / rs;
+    const int64_t threads = rp.nstrips * rp.items;
+    const int64_t grid = (threads + kThreads - 1) / kThreads;
+    if (grid > 0x7FFFFFFFLL) return 1;
+    if (above || below)
+        return launch_reg_halo<true>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
+    return launch_reg_halo<false>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
+}
+
+// Returns 1 when the streaming kernel does not apply (caller falls back).
+int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
+               const void *below, uint32_t *o_edges, uint32_t *o_eset, int word_bits,
+               int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
+               int64_t row_hi, cudaStream_t st, int thr) {
+    if (!stream_allowed()) return 1;
+    auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
+    if (nrows >= ((int64_t)1 << 31)) return 1;                     // 32-bit row arithmetic
+    StreamParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.in = (const char *)in; sp.above = (const char *)above; sp.below = (const char *)below;
+    sp.in_row_bytes = in_row_bytes;
+    sp.o_edges = o_edges; sp.o_eset = o_eset; sp.out_stride = out_stride_u32;
+    sp.nrows = nrows; sp.h = G.h; sp.w = G.w; sp.row_lo = row_lo; sp.row_hi = row_hi;
+    sp.wp = G.wp; sp.pl = G.pl; sp.lastbit = G.lastbit; sp.padmask = G.padmask;
+    sp.fillword = G.fillword;
+    sp.thr = thr;
+    sp.vst = (out_stride_u32 % 4 == 0) && al16(o_edges) && al16(o_eset);
+    int TQ, stage_target = 24 * 1024;
+    if (input_kind == 0) {
+        const int64_t wpr = (G.wp + 3) / 4 * 4;                 // words readable per row
+        TQ = wpr >= 256 ? 256 : next_pow2(wpr);
+        sp.tiles_x = (G.wp + TQ - 1) / TQ;
+        sp.contiguous = sp.tiles_x == 1 && in_row_bytes <= 8 * wpr;
+        sp.raw_pitch = sp.contiguous ? (int)in_row_bytes : 4 * TQ + 32;
+        sp.col0 = sp.contiguous ? 0 : 16;
+        sp.row_bytes_alloc = sp.contiguous ? in_row_bytes : 4 * wpr;
+    } else {
+        TQ = G.wp >= 64 ? 64 : next_pow2(G.wp);
+        sp.tiles_x = (G.wp + TQ - 1) / TQ;
+        const int64_t wr = (G.w + 15) / 16 * 16;
+        sp.contiguous = sp.tiles_x == 1 && in_row_bytes <= 2 * wr;
+        sp.raw_pitch = sp.contiguous ? (int)in_row_bytes : 32 * TQ + 32;
+        sp.col0 = sp.contiguous ? 0 : 16;
+        sp.row_bytes_alloc = sp.contiguous ? in_row_bytes : wr;
+        const int room = (sp.raw_pitch - sp.col0) / 16;
+        sp.pieces = room < 2 * TQ ? room : 2 * TQ;
+    }
+    if (sp.raw_pitch > stage_target / 3) return 1;                 // rows too wide to stage
+    sp.log_tq = ilog2(TQ);
+    int R = stage_target / sp.raw_pitch - 2;
+    const int64_t rows = row_hi - row_lo;
+    if (R > rows) R = (int)rows;
+    if (R < 1) R = 1;
+    sp.R = R;
+    sp.ntiles = ((rows + R - 1) / R) * sp.tiles_x;
+    sp.stage_bytes = ((R + 2) * sp.raw_pitch + 127) / 128 * 128;
+    sp.stages = 4;
+    size_t smem = (size_t)sp.stages * sp.stage_bytes + 8 * sp.stages;
+    if (input_kind == 1) smem += (size_t)(R + 2) * (TQ + 8) * 4;
+    if (smem > 110 * 1024) return 1;
+    if (input_kind == 1) return launch_stream_kind<kSU8>(sp, smem, st);
+    return word_bits == 64 ? launch_stream_kind<kSP64>(sp, smem, st)
+                           : launch_stream_kind<kSP32>(sp, smem, st);
+}
+
+// Shared driver of every fused-edge entry point.
+int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *above,
+               const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
+               uint32_t *o_packed, int word_bits, int64_t out_stride_words, int64_t n, int64_t h,
+               int64_t w, int fill_bit, int64_t row_lo, int64_t row_hi, void *stream, int thr) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, fill_bit);
+    if (rc) return rc;
+    if (n == 0) return BE_OK;
+    if (in == nullptr) return fail(BE_EINVAL, "input is NULL");
+    if (input_kind != 0 && input_kind != 1)
+        return fail(BE_EINVAL, "input_kind must be 0 (packed) or 1 (uint8)");
+    if ((rc = check_stride(G, out_stride_words, "output"))) return rc;
+    uint32_t *outs[7] = {o_edges, o_eset, o_side[0], o_side[1], o_side[2], o_side[3], o_packed};
+    int any = 0;
+    for (int i = 0; i < 7; ++i) {
+        if (outs[i] == nullptr) continue;
+        any = 1;
+        if ((rc = check_ptr(outs[i], word_bits, "output"))) return rc;
+        if ((const void *)outs[i] == in) return fail(BE_EINVAL, "output aliases the input");
+    }
+    if (!any) return fail(BE_EINVAL, "no output requested");
+    if ((above || below) && n != 1)
+        return fail(BE_EINVAL, "halo rows require a single slab (n == 1)");
+    const int64_t nrows = n * h;
+    if (row_lo < 0 || row_hi > nrows || row_lo > row_hi)
+        return fail(BE_EINVAL, "row range [%lld, %lld) outside [0, %lld)", (long long)row_lo,
+                    (long long)row_hi, (long long)nrows);
+    if (row_lo == row_hi) return BE_OK;
+
+    TileParams tp;
+    memset(&tp, 0, sizeof(tp));
+    tp.in = in; tp.above = above; tp.below = below;
+    tp.o_edges = o_edges; tp.o_eset = o_eset;
+    for (int s = 0; s < 4; ++s) tp.o_side[s] = o_side[s];
+    tp.o_packed = o_packed;
+    // strides in uint32 units for packed data
+    tp.out_stride = word_bits == 64 ? 2 * out_stride_words : out_stride_words;
+    tp.nrows = nrows; tp.h = h; tp.w = w; tp.row_lo = row_lo; tp.row_hi = row_hi;
+    tp.wp = G.wp; tp.pl = G.pl; tp.lastbit = G.lastbit; tp.padmask = G.padmask;
+    tp.fillword = G.fillword; tp.swap = G.swap;
+    if (thr < 0 || thr > 255) return fail(BE_EINVAL, "threshold must be 0..255, got %d", thr);
+    tp.thr = thr;
+
+    // tile shape: TQ pixel words (power of two <= 64) x R rows, ~16 KB of
+    // packed input or ~32 KB of uint8 input per CTA, smem <= 48 KB.
+    const int TQ = G.wp <= 64 ? next_pow2(G.wp) : 64;
+    const int64_t words_per_tile = input_kind == 1 ? 1024 : 4096;
+    int64_t R = words_per_tile / TQ;
+    const int64_t smem_cap_rows = (48 * 1024) / ((TQ + 8) * 4 + 1) - 2;
+    while (R > smem_cap_rows) R >>= 1;
+    const int64_t rows = row_hi - row_lo;
+    while (R > 1 && R / 2 >= rows) R >>= 1;
+    if (R < 1) R = 1;
+    tp.log_tq = ilog2(TQ);
+    tp.log_r = ilog2((int)R);
+    tp.tiles_x = (G.wp + TQ - 1) / TQ;
+
+    cudaStream_t st = S(stream);
+    const bool only_edges = !o_side[0] && !o_side[1] && !o_side[2] && !o_side[3] && !o_packed;
+    if (input_kind == 0) {
+        if ((rc = check_ptr(in, word_bits, "input"))) return rc;
+        if ((rc = check_stride(G, in_stride, "input"))) return rc;
+        if (above && (rc = check_ptr(above, word_bits, "above halo"))) return rc;
+        if (below && (rc = check_ptr(below, word_bits, "below halo"))) return rc;
+        tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
+        rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset, o_side,
+                     o_packed, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
+        if (rc != 1) return rc;
+        if (only_edges) {
+            rc = try_stream(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
+                            word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
+            if (rc != 1) return rc;
+        }
+        bool vec = TQ >= 4 && (tp.in_stride % 4) == 0 && ((uintptr_t)in % 16) == 0 &&
+                   (!above || ((uintptr_t)above % 16) == 0) &&
+                   (!below || ((uintptr_t)below % 16) == 0);
+        if (!vec) return launch_tile<kPScalar>(tp, rows, st);
+        return word_bits == 64 ? launch_tile<kP64Vec>(tp, rows, st)
+                               : launch_tile<kP32Vec>(tp, rows, st);
+    }
+    if (in_stride < w) return fail(BE_EINVAL, "input row stride %lld bytes < width %lld",
+                                   (long long)in_stride, (long long)w);
+    tp.in_stride = in_stride;
+    rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, o_side, o_packed,
+                 tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
+    if (rc != 1) return rc;
+    if (only_edges && word_bits == 32) {
+        rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
+                        G, nrows, row_lo, row_hi, st, thr);
+        if (rc != 1) return rc;
+    }
+    bool vec = (in_stride % 16) == 0 && ((uintptr_t)in % 16) == 0 &&
+               (!above || ((uintptr_t)above % 16) == 0) && (!below || ((uintptr_t)below % 16) == 0);
+    return vec ? launch_tile<kU8Vec>(tp, rows, st) : launch_tile<kU8Byte>(tp, rows, st);
+}
+
+}  // namespace capi
+}  // namespace bitedge
+
+extern "C" {
+
+int be_edges_general(const void *in, int input_kind, int64_t in_row_stride,
+                     const void *above_or_null, const void *below_or_null, const be_outputs *outs,
+                     int word_bits, int64_t out_row_stride_words, int64_t n, int64_t h, int64_t w,
+                     int fill_bit, int64_t row_lo, int64_t row_hi, void *stream) {
+    if (outs == nullptr) return fail(BE_EINVAL, "outputs is NULL");
+    uint32_t *side[4] = {(uint32_t *)outs->side[0], (uint32_t *)outs->side[1],
+                         (uint32_t *)outs->side[2], (uint32_t *)outs->side[3]};
+    return edges_impl(in, input_kind, in_row_stride, above_or_null, below_or_null,
+                      (uint32_t *)outs->edges, (uint32_t *)outs->edgeset, side,
+                      (uint32_t *)outs->packed, word_bits, out_row_stride_words, n, h, w, fill_bit,
+                      row_lo, row_hi, stream);
+}
+
+static int edge_packed(const void *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                       int64_t stride, int fill_bit, int emit_edgeset, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t *o = (uint32_t *)out;
+    return edges_impl(in, 0, stride, nullptr, nullptr, emit_edgeset ? nullptr : o,
+                      emit_edgeset ? o : nullptr, side, nullptr, word_bits, stride, n, h, w,
+                      fill_bit, 0, n * h, stream);
+}
+
+int be_edge_packed_u32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream) {
+    return edge_packed(in, out, 32, n, h, w, row_stride_words, fill_bit, emit_edgeset, stream);
+}
+
+int be_edge_packed_u64(const uint64_t *in, uint64_t *out, int64_t n, int64_t h, int64_t w,
+                       int64_t row_stride_words, int fill_bit, int emit_edgeset, void *stream) {
+    return edge_packed(in, out, 64, n, h, w, row_stride_words, fill_bit, emit_edgeset, stream);
+}
+
+int be_pack_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int fill_bit,
+                    uint32_t *packed_in_or_null, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, packed_in_or_null,
+                      32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream);
+}
+
+int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
+                            const uint32_t *below_or_null, uint32_t *out, int64_t rows, int64_t w,
+                            int64_t row_stride_words, int fill_bit, int64_t row_lo, int64_t row_hi,
+                            void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(slab, 0, row_stride_words, above_or_null, below_or_null, out, nullptr, side,
+                      nullptr, 32, row_stride_words, 1, rows, w, fill_bit, row_lo, row_hi, stream);
+}
+
+int be_pack_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+               int64_t in_row_stride, int64_t out_row_stride_words, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
+                      (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
+                      stream);
+}
+
+int be_threshold_edge_u8(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                         int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                         int fill_bit, uint32_t *binary_or_null, void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, out, nullptr, side, binary_or_null,
+                      32, out_row_stride_words, n, h, w, fill_bit, 0, n * h, stream, threshold);
+}
+
+int be_threshold_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,
+                    int64_t in_row_stride, int64_t out_row_stride_words, int threshold,
+                    void *stream) {
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (out == nullptr && n != 0) return fail(BE_EINVAL, "output is NULL");
+    return edges_impl(in, 1, in_row_stride, nullptr, nullptr, nullptr, nullptr, side,
+                      (uint32_t *)out, word_bits, out_row_stride_words, n, h, w, 1, 0, n * h,
+                      stream, threshold);
+}
+
+}  // extern "C"

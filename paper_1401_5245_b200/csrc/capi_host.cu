@@ -1,0 +1,160 @@
+// capi_host.cu -- host-buffer pipelines (the end-to-end path), CUDA IPC for
+// peer-memory halos, and the ABI's bookkeeping entry points.  Owns the library's
+// only state: a thread-local error string and launch counter.
+#include "capi_internal.cuh"
+
+using namespace bitedge;
+using namespace bitedge::capi;
+
+namespace bitedge {
+namespace capi {
+thread_local char g_err[512];
+thread_local int64_t g_launches = 0;
+}  // namespace capi
+}  // namespace bitedge
+
+extern "C" {
+
+const char *be_last_error(void) { return g_err; }
+int be_abi_version(void) { return BE_ABI_VERSION; }
+int64_t be_launch_count(void) { return g_launches; }
+
+// ---- peer-memory halos: CUDA IPC export / import of a device buffer --------
+typedef int (*cuMemGetAddressRange_t)(unsigned long long *, size_t *, unsigned long long);
+
+int be_ipc_export(const void *dev_ptr, void *handle_out, int64_t *offset_out) {
+    if (dev_ptr == nullptr || handle_out == nullptr || offset_out == nullptr)
+        return fail(BE_EINVAL, "NULL argument");
+    // the IPC handle names the whole allocation: find its base through the driver
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr)
+        return fail(e != cudaSuccess ? (int)e : BE_EINVAL, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (((cuMemGetAddressRange_t)fn)(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return fail(BE_EINVAL, "pointer is not a device allocation");
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((uintptr_t)dev_ptr - base);
+    return BE_OK;
+}
+
+int be_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out) {
+    if (handle == nullptr || dev_ptr_out == nullptr) return fail(BE_EINVAL, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *dev_ptr_out = (char *)base + offset;
+    return BE_OK;
+}
+
+int be_ipc_close(void *dev_ptr, int64_t offset) {
+    if (dev_ptr == nullptr) return fail(BE_EINVAL, "NULL argument");
+    cudaError_t e = cudaIpcCloseMemHandle((char *)dev_ptr - offset);
+    if (e != cudaSuccess) return fail((int)e, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return BE_OK;
+}
+
+int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
+                  int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
+                  int64_t chunk_images, void *stream0, void *stream1, int blocking) {
+    Geometry G;
+    int rc = make_geometry(G, 32, n, h, w, fill_bit);
+    if (rc) return rc;
+    if (n == 0) return BE_OK;
+    if (!host_in || !host_out || !dev_in || !dev_out || !dev_in[0] || !dev_in[1] || !dev_out[0] ||
+        !dev_out[1])
+        return fail(BE_EINVAL, "host / device buffers must not be NULL");
+    if (input_kind != 0 && input_kind != 1)
+        return fail(BE_EINVAL, "input_kind must be 0 (packed u32) or 1 (uint8)");
+    if (chunk_images < 1) return fail(BE_EINVAL, "chunk_images must be >= 1");
+    const int64_t wp = G.wp;
+    const size_t in_img = (size_t)h * (input_kind == 1 ? (size_t)w : (size_t)wp * 4);
+    const size_t out_img = (size_t)h * wp * 4;
+    cudaStream_t ss[2] = {S(stream0), S(stream1)};
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    // chunk c runs entirely on stream c % 2: H2D -> kernel -> D2H.  In-stream
+    // order protects the reuse of buffer c % 2 by chunk c + 2, and the two
+    // streams let one chunk's H2D overlap the other's kernel and D2H.
+    for (int64_t c = 0, lo = 0; lo < n; ++c, lo += chunk_images) {
+        const int64_t k = (n - lo) < chunk_images ? (n - lo) : chunk_images;
+        const int b = (int)(c & 1);
+        cudaError_t e = cudaMemcpyAsync(dev_in[b], (const char *)host_in + lo * in_img, k * in_img,
+                                        cudaMemcpyHostToDevice, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
+        rc = edges_impl(dev_in[b], input_kind, input_kind == 1 ? w : wp, nullptr, nullptr,
+                        dev_out[b], nullptr, side, nullptr, 32, wp, k, h, w, fill_bit, 0, k * h,
+                        ss[b]);
+        if (rc) return rc;
+        e = cudaMemcpyAsync((char *)host_out + lo * out_img, dev_out[b], k * out_img,
+                            cudaMemcpyDeviceToHost, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "D2H: %s", cudaGetErrorString(e));
+    }
+    if (blocking) {
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaStreamSynchronize(ss[b]);
+            if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+        }
+    }
+    return BE_OK;
+}
+
+int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
+                       int64_t w, int fill_bit, int halo_flags, void *const dev_in[2],
+                       uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,
+                       void *stream1, int blocking) {
+    Geometry G;
+    int rc = make_geometry(G, 32, 1, h, w, fill_bit);
+    if (rc) return rc;
+    if (!host_in || !host_out || !dev_in || !dev_out || !dev_in[0] || !dev_in[1] || !dev_out[0] ||
+        !dev_out[1])
+        return fail(BE_EINVAL, "host / device buffers must not be NULL");
+    if (input_kind != 0 && input_kind != 1)
+        return fail(BE_EINVAL, "input_kind must be 0 (packed u32) or 1 (uint8)");
+    if (chunk_rows < 1) return fail(BE_EINVAL, "chunk_rows must be >= 1");
+    if (halo_flags & ~3) return fail(BE_EINVAL, "halo_flags must be a combination of 1 and 2");
+    const int64_t wp = G.wp;
+    const size_t in_row = input_kind == 1 ? (size_t)w : (size_t)wp * 4;
+    const size_t out_row = (size_t)wp * 4;
+    const bool has_above = halo_flags & 1, has_below = halo_flags & 2;
+    // row r of the image is host row r + has_above; rows -1 / h exist iff flagged
+    const char *hin = (const char *)host_in + (has_above ? in_row : 0);
+    cudaStream_t ss[2] = {S(stream0), S(stream1)};
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    // chunk c on stream c % 2: H2D of rows [r0-1, r1+1) -> halo kernel on rows
+    // [r0, r1) -> D2H; in-stream order protects buffer c % 2 for chunk c + 2
+    for (int64_t c = 0, r0 = 0; r0 < h; ++c, r0 += chunk_rows) {
+        const int64_t r1 = (h - r0) < chunk_rows ? h : r0 + chunk_rows;
+        const bool up = r0 > 0 || has_above, dn = r1 < h || has_below;
+        const int64_t lo = up ? r0 - 1 : r0, hi = dn ? r1 + 1 : r1;
+        const int b = (int)(c & 1);
+        char *din = (char *)dev_in[b];
+        cudaError_t e = cudaMemcpyAsync(din, hin + lo * (int64_t)in_row, (hi - lo) * in_row,
+                                        cudaMemcpyHostToDevice, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
+        const char *slab = din + (r0 - lo) * in_row;
+        const void *above = up ? (const void *)din : nullptr;
+        const void *below = dn ? (const void *)(slab + (r1 - r0) * in_row) : nullptr;
+        rc = edges_impl(slab, input_kind, input_kind == 1 ? w : wp, above, below, dev_out[b],
+                        nullptr, side, nullptr, 32, wp, 1, r1 - r0, w, fill_bit, 0, r1 - r0, ss[b]);
+        if (rc) return rc;
+        e = cudaMemcpyAsync((char *)host_out + r0 * out_row, dev_out[b], (r1 - r0) * out_row,
+                            cudaMemcpyDeviceToHost, ss[b]);
+        if (e != cudaSuccess) return fail((int)e, "D2H: %s", cudaGetErrorString(e));
+    }
+    if (blocking) {
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaStreamSynchronize(ss[b]);
+            if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+        }
+    }
+    return BE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// capi_p4.cu -- PBM P4 payloads at the kernel boundary:
+// decode / encode kernels and the fused P4 -> edges -> P4 path through K1.
+#include "capi_internal.cuh"
+#include "edge_reg.cuh"
+
+using namespace bitedge;
+using namespace bitedge::capi;
+
+namespace bitedge {
+namespace capi {
+
+// ---------------------------------------------------------------- PBM P4 codec (F1)
+// P4 payload rows are ceil(w/8) bytes, MSB-first, 1 = black;
+// the rasters here are MSB-first words with 1 = white and padding 1.
+
+__global__ void p4_decode_kernel(const uint8_t *__restrict__ p4, uint32_t *__restrict__ out,
+                                 WordGeom g, int64_t rb, int64_t out_stride) {
+    const int64_t total = g.nrows * g.wp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / g.wp;
+        const int pw = (int)(t - row * g.wp);
+        const uint8_t *r = p4 + row * rb;
+        uint32_t v = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t j = (int64_t)pw * 4 + k;
+            v = (v << 8) | (j < rb ? r[j] : 0u);
+        }
+        out[row * out_stride + (pw ^ g.swap)] = force_pad(g, pw, ~v);
+    }
+}
+
+__global__ void p4_encode_kernel(const uint32_t *__restrict__ in, uint8_t *__restrict__ p4,
+                                 WordGeom g, int64_t rb, int64_t in_stride) {
+    const int64_t total = g.nrows * rb;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / rb;
+        const int64_t j = t - row * rb;
+        const int pw = (int)(j >> 2);
+        uint32_t v = in[row * in_stride + (pw ^ g.swap)];
+        if (pw == g.pl) v |= g.padmask;            // padding -> 0 on disk
+        p4[t] = (uint8_t)(~(v >> (24 - 8 * (j & 3))));
+    }
+}
+
+}  // namespace capi
+}  // namespace bitedge
+
+
+// ================================================================ C ABI
+
+extern "C" int be_p4_decode(const uint8_t *p4, void *out, int word_bits, int64_t n, int64_t h,
+                            int64_t w, int64_t out_row_stride_words, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, 1);
+    if (rc) return rc;
+    if ((rc = check_stride(G, out_row_stride_words, "output"))) return rc;
+    if (n == 0) return BE_OK;
+    if (p4 == nullptr) return fail(BE_EINVAL, "P4 payload is NULL");
+    if ((rc = check_ptr(out, word_bits, "output"))) return rc;
+    WordGeom g = word_geom(G, out_row_stride_words);
+    const int64_t rb = (w + 7) / 8;
+    p4_decode_kernel<<<grid_for(g.nrows * g.wp), 256, 0, S(stream)>>>(p4, (uint32_t *)out, g, rb,
+                                                                       g.stride);
+    return cuda_check("p4_decode_kernel");
+}
+
+extern "C" int be_p4_encode(const void *in, uint8_t *p4, int word_bits, int64_t n, int64_t h,
+                            int64_t w, int64_t in_row_stride_words, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, word_bits, n, h, w, 1);
+    if (rc) return rc;
+    if ((rc = check_stride(G, in_row_stride_words, "input"))) return rc;
+    if (n == 0) return BE_OK;
+    if (p4 == nullptr) return fail(BE_EINVAL, "P4 payload is NULL");
+    if ((rc = check_ptr(in, word_bits, "input"))) return rc;
+    WordGeom g = word_geom(G, in_row_stride_words);
+    const int64_t rb = (w + 7) / 8;
+    p4_encode_kernel<<<grid_for(g.nrows * rb), 256, 0, S(stream)>>>((const uint32_t *)in, p4, g,
+                                                                     rb, g.stride);
+    return cuda_check("p4_encode_kernel");
+}
+
+extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int64_t h, int64_t w,
+                           int fill_bit, uint32_t *scratch_or_null, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, 32, n, h, w, fill_bit);
+    if (rc) return rc;
+    if (n == 0) return BE_OK;
+    if (p4_in == nullptr || p4_out == nullptr) return fail(BE_EINVAL, "P4 buffers must not be NULL");
+    if ((const void *)p4_in == (const void *)p4_out) return fail(BE_EINVAL, "output aliases the input");
+    const int64_t rb = (w + 7) / 8;
+    cudaStream_t st = S(stream);
+    auto al = [](const void *p, int a) { return ((uintptr_t)p % a) == 0; };
+    // fused path: P4 rows are whole 16-byte chunks -> K1 reads and writes P4 directly
+    if (rb % 16 == 0 && al(p4_in, 16) && al(p4_out, 16) && !getenv("BITEDGE_P4_UNFUSED") &&
+        n * h < ((int64_t)1 << 31)) {
+        RegParams rp;
+        memset(&rp, 0, sizeof(rp));
+        rp.in = (const char *)p4_in; rp.in_row_bytes = rb;
+        rp.o_edges = (uint32_t *)p4_out; rp.out_stride = rb / 4;
+        rp.nrows = n * h; rp.row_lo = 0; rp.row_hi = n * h;
+        rp.h = (uint32_t)h; rp.w = w; rp.wp = G.wp; rp.pl = G.pl;
+        rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
+        rp.thr = 1;
+        const bool v8 = rb % 32 == 0 && al(p4_in, 32) && al(p4_out, 32);
+        const int cw = v8 ? 8 : 4;
+        rp.items = (G.wp + cw - 1) / cw;
+        rp.vst = 1;
+        // 2-row strips for small rasters (twice the threads in flight), as try_reg does
+        const bool big = ((n * h + 3) / 4) * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
+        const int rs = big ? 4 : 2;
+        rp.nstrips = (n * h + rs - 1) / rs;
+        const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
+        if (grid <= 0x7FFFFFFFLL) {
+            if (cw == 8 && rs == 4)
+                launch_k(edge_reg_packed_kernel<0, 4, 8, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            else if (cw == 8)
+                launch_k(edge_reg_packed_kernel<0, 2, 8, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            else if (rs == 4)
+                launch_k(edge_reg_packed_kernel<0, 4, 4, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            else
+                launch_k(edge_reg_packed_kernel<0, 2, 4, kOutEdges, false, true>, (unsigned)grid, 0,
+                         st, rp);
+            return cuda_check("edge_reg_packed_kernel<P4>");
+        }
+    }
+    // general path: decode -> K1 -> encode through caller scratch (2 word rasters)
+    if (scratch_or_null == nullptr)
+        return fail(BE_EINVAL, "unaligned P4 rows (ceil(w/8) %% 16 != 0) need a scratch buffer of "
+                               "2 * n * h * ceil(w/32) words");
+    const int64_t words = n * h * G.wp;
+    uint32_t *dec = scratch_or_null, *edg = scratch_or_null + words;
+    if ((rc = be_p4_decode(p4_in, dec, 32, n, h, w, G.wp, stream))) return rc;
+    if ((rc = be_edge_packed_u32(dec, edg, n, h, w, G.wp, fill_bit, 0, stream))) return rc;
+    return be_p4_encode(edg, p4_out, 32, n, h, w, G.wp, stream);
+}
