@@ -67,25 +67,34 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 // Launch helpers: dispatch the runtime choices onto template parameters.
 template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
+    K1Div dv;
+    if (!k1_setup(rp, dv)) return 1;   // > 2^32 threads or rows: tile kernel
     if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
-        if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
-        else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
-        else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+        if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
+        else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp, dv);
+        else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         (void)cw;
     } else {
-        if (!swap && rs == 2) {
+        // whole 8-word items with no padding (w % 256 == 0: C3, C4): the tail-free kernels
+        const bool aligned = OUT == kOutEdges && !swap && cw == 8 && rp.w % 256 == 0 &&
+                             !getenv("BITEDGE_K1_GENERIC");
+        if (aligned && rs == 2) {
+            launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
+        } else if (aligned && rs == 4) {
+            launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
+        } else if (!swap && rs == 2) {
             // (128-thread CTAs for C3's single wave: +2 % overlapped, -1 % serial; not taken)
-            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp);
-            else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp);
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp, dv);
         } else if (!swap && rs == 8) {
-            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp);
-            else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp);
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 8, 8, OUT, HALO>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<0, 8, 4, OUT, HALO>, grid, 0, st, rp, dv);
         } else if (swap) {
-            if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp);
-            else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp);
+            if (cw == 8) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         } else {
-            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp);
-            else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp);
+            if (cw == 8) launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         }
     }
     return cuda_check("edge_reg_packed_kernel");

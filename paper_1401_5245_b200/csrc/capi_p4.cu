@@ -114,19 +114,27 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
         const int rs = big ? 4 : 2;
         rp.nstrips = (n * h + rs - 1) / rs;
         const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
-        if (grid <= 0x7FFFFFFFLL) {
-            if (cw == 8 && rs == 4)
+        K1Div dv;
+        if (grid <= 0x7FFFFFFFLL && k1_setup(rp, dv)) {
+            const bool aligned = cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
+            if (aligned && rs == 4)
+                launch_k(edge_reg_packed_kernel<0, 4, 8, kOutEdges, false, true, true>, (unsigned)grid,
+                         0, st, rp, dv);
+            else if (aligned)
+                launch_k(edge_reg_packed_kernel<0, 2, 8, kOutEdges, false, true, true>, (unsigned)grid,
+                         0, st, rp, dv);
+            else if (cw == 8 && rs == 4)
                 launch_k(edge_reg_packed_kernel<0, 4, 8, kOutEdges, false, true>, (unsigned)grid, 0,
-                         st, rp);
+                         st, rp, dv);
             else if (cw == 8)
                 launch_k(edge_reg_packed_kernel<0, 2, 8, kOutEdges, false, true>, (unsigned)grid, 0,
-                         st, rp);
+                         st, rp, dv);
             else if (rs == 4)
                 launch_k(edge_reg_packed_kernel<0, 4, 4, kOutEdges, false, true>, (unsigned)grid, 0,
-                         st, rp);
+                         st, rp, dv);
             else
                 launch_k(edge_reg_packed_kernel<0, 2, 4, kOutEdges, false, true>, (unsigned)grid, 0,
-                         st, rp);
+                         st, rp, dv);
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }

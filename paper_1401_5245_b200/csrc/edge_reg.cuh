@@ -118,59 +118,90 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
 //   out = c & ~(pi(~Ln & ~Rn) & u & d)      (1 = black edge pixel)
 __device__ __forceinline__ uint32_t p4_pi(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
-template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false>
+// Unsigned 32-bit division by a launch constant without the IDIV sequence
+// (Granlund-Montgomery): q = (umulhi(n, m) + n) >> l, exact for all n < 2^32.
+struct FastDiv {
+    uint32_t m;
+    int l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {       // host; d >= 1
+    int l = 0;
+    while (((uint64_t)1 << l) < d) ++l;
+    const uint64_t m = ((((uint64_t)1 << l) - d) << 32) / d + 1;
+    return {(uint32_t)m, l};
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, FastDiv f) {
+    return (uint32_t)(((uint64_t)__umulhi(n, f.m) + n) >> f.l);
+}
+
+// K1 per-launch constants beyond RegParams: the thread -> (strip, item) and
+// row -> row-in-image divisions.  Valid when strips * items and nrows < 2^32
+// (k1_setup checks; the callers fall back to the tile kernel otherwise).
+struct K1Div {
+    FastDiv items, h;
+};
+inline bool k1_setup(const RegParams &p, K1Div &d) {
+    if (p.nstrips * (int64_t)p.items + kThreads >= ((int64_t)1 << 32) || p.row_hi >= ((int64_t)1 << 32))
+        return false;
+    d.items = make_fastdiv((uint32_t)p.items);
+    d.h = make_fastdiv(p.h);
+    return true;
+}
+
+// ALIGNED: w % (32 * CW) == 0 (C3, C4 and P4 at those sizes) -- every item is
+// whole, there are no padding bits and the only border work at the right edge
+// is the fill word to the right of a row's last item, so the per-word tail
+// test (pixel w-1 fill, padding force) is compiled out.
+template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false>
 __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
-edge_reg_packed_kernel(const RegParams p) {
+edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
     pdl_wait();
     pdl_trigger();
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // 128 or 256 per CTA
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;   // < 2^32 (k1_setup)
     const int lane = threadIdx.x & 31;
-    const int64_t strip = t / p.items;
-    const int c = (int)(t - strip * p.items);
+    const uint32_t strip = fdiv(t, dv.items);
+    const int c = (int)(t - strip * (uint32_t)p.items);
     const bool live = strip < p.nstrips;
-    const int64_t g0 = p.row_lo + strip * RS;
+    const int64_t g0 = p.row_lo + (int64_t)strip * RS;
     const int pw0 = CW * c;
     const uint32_t fw = p.fillword;
     const int64_t rb = p.in_row_bytes;
 
-    // ---- issue every load of the strip up front; staged row i = global row g0-1+i
-    const char *base = p.in + (g0 - 1) * rb + 4 * pw0;
-    const int i_lo = g0 == 0 ? 1 : 0;
-    const int64_t lim = p.nrows - (g0 - 1);                 // rows i < lim exist
+    // ---- issue every load of the strip up front; staged row i = global row g0-1+i.
+    // Rows outside [0, nrows) are loaded from a clamped (valid) address: their
+    // values are never used -- the first/last row of every image takes the fill
+    // (top / bot below) unless a halo pointer supplies the neighbour row -- so
+    // no predicates or fill moves are needed here.
+    const char *col = p.in + 4 * pw0;
+    const int64_t last = p.nrows - 1;
     const bool need_l = live && c > 0 && lane == 0;
     const bool need_r = live && c + 1 < p.items && lane == 31;
     uint32_t v[RS + 2][CW];
     uint32_t lwx[RS], rwx[RS];
 #pragma unroll
     for (int i = 0; i < RS + 2; ++i) {
-        const char *ptr = base + i * rb;
-        bool ok = live && i >= i_lo && i < lim;
+        const int64_t gi = g0 - 1 + i;
+        const char *ptr = col + min(max(gi, (int64_t)0), last) * rb;
         if (HALO) {
-            if (i == 0 && g0 == 0 && p.above) { ptr = p.above + 4 * pw0; ok = live; }
-            if (i == lim && p.below) { ptr = p.below + 4 * pw0; ok = live; }
+            if (i == 0 && gi < 0 && p.above) ptr = p.above + 4 * pw0;
+            if (i >= 1 && gi == p.nrows && p.below) ptr = p.below + 4 * pw0;   // partial last strip too
         }
-        if (ok) {
-            load_chunk<CW>(ptr, v[i]);               // P4: raw bytes, converted per use
-        } else {
-#pragma unroll
-            for (int q = 0; q < CW; ++q) v[i][q] = P4 ? ~fw : fw;
-        }
+        load_chunk<CW>(ptr, v[i]);                   // P4: raw bytes, converted per use
         if (i >= 1 && i <= RS) {
-            lwx[i - 1] = fw;
-            rwx[i - 1] = 0u;
-            if (ok && need_l) lwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? -2 : -1));
-            if (ok && need_r) rwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? CW + 1 : CW));
-            if (P4) {                                // pixel order, black polarity
-                lwx[i - 1] = (ok && need_l) ? p4_pi(lwx[i - 1]) : ~fw;
-                rwx[i - 1] = (ok && need_r) ? p4_pi(rwx[i - 1]) : 0xFFFFFFFFu;
-            }
+            // P4: raw bytes, byte-swapped at use (converting here would make the
+            // warp wait for this load before issuing the next rows' loads); the
+            // defaults (black polarity) are invariant under the byte swap
+            lwx[i - 1] = P4 ? ~fw : fw;
+            rwx[i - 1] = P4 ? 0xFFFFFFFFu : 0u;
+            if (need_l) lwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? -2 : -1));
+            if (need_r) rwx[i - 1] = __ldg((const uint32_t *)ptr + (SWAP ? CW + 1 : CW));
         }
     }
 
     const bool tail = pw0 + CW - 1 >= p.pl;
     const int nst = min(CW, p.wp - pw0);
     const uint32_t pad_pi = P4 ? p4_pi(p.padmask) : 0u;
-    uint32_t y = live ? (uint32_t)(g0 % p.h) : 0u;
+    uint32_t y = live ? (uint32_t)g0 - fdiv((uint32_t)g0, dv.h) * p.h : 0u;
     int64_t o = g0 * p.out_stride + pw0;
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
@@ -184,67 +215,54 @@ edge_reg_packed_kernel(const RegParams p) {
         }
         uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cc[CW - 1], 1);
         uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
-        if (lane == 0) lw = lwx[r];
-        if (lane == 31) rw = rwx[r];
+        if (lane == 0) lw = P4 ? p4_pi(lwx[r]) : lwx[r];
+        if (lane == 31) rw = P4 ? p4_pi(rwx[r]) : rwx[r];
         if (c == 0) lw = P4 ? ~fw : fw;
+        if (ALIGNED && c + 1 == p.items) rw = P4 ? ~fw : fw;   // pixel w is outside: the fill
         const int64_t g = g0 + r;
         if (live && g < p.row_hi) {
             const bool top = (y == 0) && !(HALO && p.above);
             const bool bot = (y == p.h - 1) && !(HALO && p.below);
-            uint32_t ve[CW], vs[CW];
-            constexpr int NA = OUT == kOutAll ? CW : 1;
-            uint32_t lnv[NA], rnv[NA], uv[NA], dv[NA], fv[NA];   // kOutAll only
-#pragma unroll
-            for (int q = 0; q < CW; ++q) {
+            const uint32_t ufill = P4 ? ~fw : fw;
+            // Neighbour planes of word q (pixel order; P4: black polarity) with the
+            // fill at pixel w-1 and the padding force on the row's last item.
+            auto planes = [&](int q, uint32_t &ln, uint32_t &rn, uint32_t &u, uint32_t &d,
+                              uint32_t &f) {
                 const uint32_t left = q == 0 ? lw : cc[q - 1];
                 const uint32_t right = q == CW - 1 ? rw : cc[q + 1];
-                const uint32_t ln = __funnelshift_r(cc[q], left, 1);
-                uint32_t rn = __funnelshift_l(right, cc[q], 1);
-                uint32_t f = 0u;
-                if (P4) {
-                    // ln / rn are ~Ln / ~Rn here (black polarity); the padding force
-                    // is applied in the P4 byte order directly (pad_pi = pi(padmask))
-                    uint32_t fpi = 0u;
-                    if (tail) {
-                        const int pw = pw0 + q;
-                        if (pw == p.pl) {
-                            rn = (rn & ~p.lastbit) | (~fw & p.lastbit);
-                            fpi = pad_pi;
-                        } else if (pw > p.pl) {
-                            fpi = 0xFFFFFFFFu;
-                        }
-                    }
-                    const uint32_t u = top ? ~fw : cu[q];
-                    const uint32_t d = bot ? ~fw : cd[q];
-                    ve[q] = v[r + 1][q] & ~(p4_pi(ln & rn) & u & d) & ~fpi;
-                    vs[q] = 0u;
-                } else {
-                    if (tail) fix_tail(pw0 + q, p, rn, f);
-                    const uint32_t u = top ? fw : cu[q];
-                    const uint32_t d = bot ? fw : cd[q];
-                    const uint32_t a = ln | rn | u | d;
-                    ve[q ^ SWAP] = cc[q] | ~a | f;
-                    vs[q ^ SWAP] = (~cc[q] & a) | f;
-                    if (OUT == kOutAll) {
-                        lnv[q] = ln; rnv[q] = rn; uv[q] = u; dv[q] = d; fv[q] = f;
+                ln = __funnelshift_r(cc[q], left, 1);
+                rn = __funnelshift_l(right, cc[q], 1);
+                u = top ? ufill : cu[q];
+                d = bot ? ufill : cd[q];
+                f = 0u;
+                if (!ALIGNED && tail) {
+                    const int pw = pw0 + q;
+                    if (pw == p.pl) {
+                        rn = (rn & ~p.lastbit) | ((P4 ? ~fw : fw) & p.lastbit);
+                        f = P4 ? pad_pi : p.padmask;
+                    } else if (pw > p.pl) {
+                        f = 0xFFFFFFFFu;
                     }
                 }
-            }
+            };
             if constexpr (OUT == kOutAll) {
+                uint32_t lnv[CW], rnv[CW], uv[CW], dv2[CW], fv[CW];
+#pragma unroll
+                for (int q = 0; q < CW; ++q) planes(q, lnv[q], rnv[q], uv[q], dv2[q], fv[q]);
                 // one output at a time, rebuilt from the neighbour planes
                 auto put = [&](uint32_t *dst, int which) {
                     if (dst == nullptr) return;
-                    uint32_t t[CW];
+                    uint32_t tw[CW];
 #pragma unroll
                     for (int q = 0; q < CW; ++q) {
-                        const AllWords x = all_words(cc[q], lnv[q], rnv[q], uv[q], dv[q], fv[q]);
-                        t[q ^ SWAP] = which == 0 ? x.e : which == 1 ? x.s : which == 2 ? x.l
-                                    : which == 3 ? x.r : which == 4 ? x.u : which == 5 ? x.d : x.pk;
+                        const AllWords x = all_words(cc[q], lnv[q], rnv[q], uv[q], dv2[q], fv[q]);
+                        tw[q ^ SWAP] = which == 0 ? x.e : which == 1 ? x.s : which == 2 ? x.l
+                                     : which == 3 ? x.r : which == 4 ? x.u : which == 5 ? x.d : x.pk;
                     }
                     if (nst == CW && p.vst) {
-                        store_chunk<CW>(dst + o, t);
+                        store_chunk<CW>(dst + o, tw);
                     } else {
-                        for (int q = 0; q < nst; ++q) dst[o + q] = t[q];
+                        for (int q = 0; q < nst; ++q) dst[o + q] = tw[q];
                     }
                 };
                 put(p.o_edges, 0);
@@ -254,13 +272,32 @@ edge_reg_packed_kernel(const RegParams p) {
                 put(p.o_side[2], 4);
                 put(p.o_side[3], 5);
                 put(p.o_packed, 6);
-            } else if (nst == CW && p.vst) {
-                if (OUT != kOutEset) store_chunk<CW>(p.o_edges + o, ve);
-                if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + o, vs);
             } else {
-                for (int q = 0; q < nst; ++q) {
-                    if (OUT != kOutEset) p.o_edges[o + q] = ve[q];
-                    if (OUT != kOutEdges) p.o_eset[o + q] = vs[q];
+                uint32_t ve[CW], vs[CW];
+                auto word = [&](int q) {
+                    uint32_t ln, rn, u, d, f;
+                    planes(q, ln, rn, u, d, f);
+                    if (P4) {
+                        // ln / rn are ~Ln / ~Rn here (black polarity); the force is
+                        // already in P4 byte order.  out = c & ~(pi(~Ln & ~Rn) & u & d)
+                        ve[q] = v[r + 1][q] & ~(p4_pi(ln & rn) & u & d) & ~f;
+                        vs[q] = 0u;
+                    } else {
+                        const uint32_t a = ln | rn | u | d;
+                        ve[q ^ SWAP] = cc[q] | ~a | f;
+                        vs[q ^ SWAP] = (~cc[q] & a) | f;
+                    }
+                };
+#pragma unroll
+                for (int q = 0; q < CW; ++q) word(q);
+                if (nst == CW && p.vst) {
+                    if (OUT != kOutEset) store_chunk<CW>(p.o_edges + o, ve);
+                    if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + o, vs);
+                } else {
+                    for (int q = 0; q < nst; ++q) {
+                        if (OUT != kOutEset) p.o_edges[o + q] = ve[q];
+                        if (OUT != kOutEdges) p.o_eset[o + q] = vs[q];
+                    }
                 }
             }
         }

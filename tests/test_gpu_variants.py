@@ -32,6 +32,9 @@ VARIANTS = {
     "warpimg_g4": {"BITEDGE_WARPIMG_G4": "1"},
     "pdl_late": {"BITEDGE_PDL_LATE": "1"},
     "tma_warp_rsl32": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"},
+    "k1_generic": {"BITEDGE_K1_GENERIC": "1"},
+    "k1_prs2": {"BITEDGE_PRS": "2"},
+    "k1_prs8": {"BITEDGE_PRS": "8"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns

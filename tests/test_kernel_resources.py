@@ -17,6 +17,8 @@ LOG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 BUDGET = {
     "edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0E": 64,   # C3: K1 2-row, 8-word items
     "edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0E": 80,   # C4: K1 4-row, 8-word items
+    "edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb1E": 48,   # C3 tail-free: 5 CTAs/SM
+    "edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb1E": 72,   # C4 tail-free
     "edge_warp_img_kernelILi1ELi0ELi8E": 80,                 # C2: K2w, 64-px rows
     "edge_tma2_u8_kernelILi8ELi4ELi0ELb0E": 80,             # C5: K2t2 (smem caps it at 3 CTAs/SM)
     "edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb1E": 80,   # F1: P4 4-row
@@ -51,8 +53,14 @@ def test_hot_kernel_register_budget(frag, budget):
 # unrolled into every row of its strip loop, and C5 lost 47 % to instruction-
 # cache misses (676 -> 994 us) with no change in registers.
 SASS_BUDGET = {
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0EEEvNS_9RegParamsE": 950,
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0EEEvNS_9RegParamsE": 1450,
+    # K1, tail-free (w % 256 == 0) variants: C3, C4, C4 row slabs, P4 (F1)
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb1EEEvNS_9RegParamsENS_5K1DivE": 500,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb1EEEvNS_9RegParamsENS_5K1DivE": 800,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb1ELb0ELb1EEEvNS_9RegParamsENS_5K1DivE": 800,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb1ELb1EEEvNS_9RegParamsENS_5K1DivE": 850,
+    # K1 general (ragged widths)
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 950,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 1450,
     "_ZN7bitedge20edge_warp_img_kernelILi1ELi0ELi8EEEvNS_9RegParamsEil": 1550,
     "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0EEEvNS_9RegParamsEll": 2800,
 }
