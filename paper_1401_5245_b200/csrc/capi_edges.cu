@@ -68,7 +68,7 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
     K1Div dv;
-    if (!k1_setup(rp, dv)) return 1;   // > 2^32 threads or rows: tile kernel
+    if (!k1_setup(rp, dv)) return kNoKernel;   // > 2^32 threads or rows: tile kernel
     if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
         if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp, dv);
@@ -120,7 +120,7 @@ template <bool HALO>
 int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
                     cudaStream_t st) {
     if (multi_out(rp)) {          // packed input only (uint8 multi-output goes to K2t2 or tile)
-        if (input_kind == 1) return 1;
+        if (input_kind == 1) return kNoKernel;
         return launch_reg_packed<kOutAll, HALO>(rp, swap, cw, rs, grid, st);
     }
     if (input_kind == 1) {
@@ -133,7 +133,7 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
     return launch_reg_packed<kOutEdges, HALO>(rp, swap, cw, rs, grid, st);
 }
 
-// Returns 1 when the register-direct kernel does not apply (caller falls back).
+// Returns kNoKernel when the register-direct kernel does not apply (caller falls back).
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 
 // K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA).
@@ -170,10 +170,10 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
             int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
     const char *e = getenv("BITEDGE_KERNEL");
-    if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return 1;
+    if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return kNoKernel;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
-    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
-    if (G.h >= ((int64_t)1 << 31)) return 1;
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return kNoKernel;
+    if (G.h >= ((int64_t)1 << 31)) return kNoKernel;
     RegParams rp;
     memset(&rp, 0, sizeof(rp));
     rp.in = (const char *)in; rp.above = (const char *)above; rp.below = (const char *)below;
@@ -186,7 +186,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // swapped halves; it takes every such shape >= 1024 px wide, the tile kernel
     // the rest
     const bool u64_out = input_kind == 1 && G.swap;
-    if (u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"))) return 1;
+    if (u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"))) return kNoKernel;
     rp.oswap = u64_out ? 1 : 0;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
@@ -280,7 +280,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
-    if ((multi || u64_out) && input_kind == 1) return 1;   // other uint8 shapes: tile kernel
+    if ((multi || u64_out) && input_kind == 1) return kNoKernel;   // other uint8 shapes: tile kernel
     if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
@@ -345,21 +345,21 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
     const int64_t grid = (threads + kThreads - 1) / kThreads;
-    if (grid > 0x7FFFFFFFLL) return 1;
+    if (grid > 0x7FFFFFFFLL) return kNoKernel;
     if (above || below)
         return launch_reg_halo<true>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
     return launch_reg_halo<false>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);
 }
 
-// Returns 1 when the streaming kernel does not apply (caller falls back).
+// Returns kNoKernel when the streaming kernel does not apply (caller falls back).
 int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
                const void *below, uint32_t *o_edges, uint32_t *o_eset, int word_bits,
                int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
                int64_t row_hi, cudaStream_t st, int thr) {
-    if (!stream_allowed()) return 1;
+    if (!stream_allowed()) return kNoKernel;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
-    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return 1;
-    if (nrows >= ((int64_t)1 << 31)) return 1;                     // 32-bit row arithmetic
+    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return kNoKernel;
+    if (nrows >= ((int64_t)1 << 31)) return kNoKernel;                     // 32-bit row arithmetic
     StreamParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.in = (const char *)in; sp.above = (const char *)above; sp.below = (const char *)below;
@@ -390,7 +390,7 @@ int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void 
         const int room = (sp.raw_pitch - sp.col0) / 16;
         sp.pieces = room < 2 * TQ ? room : 2 * TQ;
     }
-    if (sp.raw_pitch > stage_target / 3) return 1;                 // rows too wide to stage
+    if (sp.raw_pitch > stage_target / 3) return kNoKernel;                 // rows too wide to stage
     sp.log_tq = ilog2(TQ);
     int R = stage_target / sp.raw_pitch - 2;
     const int64_t rows = row_hi - row_lo;
@@ -402,7 +402,7 @@ int try_stream(const void *in, int input_kind, int64_t in_row_bytes, const void 
     sp.stages = 4;
     size_t smem = (size_t)sp.stages * sp.stage_bytes + 8 * sp.stages;
     if (input_kind == 1) smem += (size_t)(R + 2) * (TQ + 8) * 4;
-    if (smem > 110 * 1024) return 1;
+    if (smem > 110 * 1024) return kNoKernel;
     if (input_kind == 1) return launch_stream_kind<kSU8>(sp, smem, st);
     return word_bits == 64 ? launch_stream_kind<kSP64>(sp, smem, st)
                            : launch_stream_kind<kSP32>(sp, smem, st);
@@ -476,11 +476,11 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
         tp.in_stride = word_bits == 64 ? 2 * in_stride : in_stride;
         rc = try_reg(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset, o_side,
                      o_packed, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
-        if (rc != 1) return rc;
+        if (rc != kNoKernel) return rc;
         if (only_edges) {
             rc = try_stream(in, 0, in_stride * (word_bits / 8), above, below, o_edges, o_eset,
                             word_bits, tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
-            if (rc != 1) return rc;
+            if (rc != kNoKernel) return rc;
         }
         bool vec = TQ >= 4 && (tp.in_stride % 4) == 0 && ((uintptr_t)in % 16) == 0 &&
                    (!above || ((uintptr_t)above % 16) == 0) &&
@@ -494,11 +494,11 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     tp.in_stride = in_stride;
     rc = try_reg(in, 1, in_stride, above, below, o_edges, o_eset, o_side, o_packed,
                  tp.out_stride, G, nrows, row_lo, row_hi, st, thr);
-    if (rc != 1) return rc;
+    if (rc != kNoKernel) return rc;
     if (only_edges && word_bits == 32) {
         rc = try_stream(in, 1, in_stride, above, below, o_edges, o_eset, word_bits, tp.out_stride,
                         G, nrows, row_lo, row_hi, st, thr);
-        if (rc != 1) return rc;
+        if (rc != kNoKernel) return rc;
     }
     bool vec = (in_stride % 16) == 0 && ((uintptr_t)in % 16) == 0 &&
                (!above || ((uintptr_t)above % 16) == 0) && (!below || ((uintptr_t)below % 16) == 0);

@@ -29,6 +29,11 @@ inline int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+// "this kernel does not apply, try the next one" from the kernel-selection
+// helpers: distinct from BE_OK, the negative BE_E* codes and every (positive)
+// cudaError_t, so a CUDA error is never mistaken for a fallback.
+constexpr int kNoKernel = -1000;
+
 inline int cuda_check(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
