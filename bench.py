@@ -598,6 +598,11 @@ def run_ours(args):
                "h2d_bytes_per_step": moved[0], "d2h_bytes_per_step": moved[1],
                "steps": e2e_steps, "ms_per_step": ems / e2e_steps,
                "windows_gpx_s": [round(px_e2e * per_win / (m / 1e3) / 1e9, 2) for m in wms]}
+        # this box's PCIe context for the number above: a plain pinned H2D copy
+        # (the e2e step's dominant transfer) timed on the same GPU right after
+        h2d = h2d_rate(hin, dev)
+        e2e["pcie_h2d_gbs"] = round(h2d, 2)
+        e2e["h2d_only_floor_gpx_s"] = round(px_e2e / (pipe.h2d_bytes / (h2d * 1e9)) / 1e9, 2)
 
     # ---- parity gate on the measured output (before reporting a number)
     parity = None
@@ -649,6 +654,25 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def h2d_rate(hin, dev, total=2 << 30):
+    """GB/s of plain pinned host -> device copies of (up to 64 MiB of) `hin`,
+    ~2 GB timed with CUDA events: the PCIe rate the e2e number runs against."""
+    src = hin.reshape(-1).view(torch.uint8)
+    src = src[: min(src.numel(), 64 << 20)]
+    dst = torch.empty(src.numel(), dtype=torch.uint8, device=dev)
+    reps = max(4, total // max(1, src.numel()))
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    return src.numel() * reps / (a.elapsed_time(b) / 1e3) / 1e9
 
 
 def gate(cfg, inp, out, kind, w):
