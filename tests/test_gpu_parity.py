@@ -376,14 +376,19 @@ def test_beyond_4gib_packed(wb, cuda_dev):
 
 # ---------------------------------------------------------------- row sharding (K3)
 
+@pytest.mark.parametrize("W", [2048 + 96, 2048, 8192])   # ragged, and K1's tail-free (w % 256 == 0) kernels
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
-def test_row_slabs_with_halos_equal_whole(cuda_dev, G):
+@pytest.mark.parametrize("prs", ["", "4"])    # K1 strip height: size-chosen, or forced 4 rows
+def test_row_slabs_with_halos_equal_whole(cuda_dev, G, W, prs, monkeypatch):
     import torch
+
+    if prs:
+        monkeypatch.setenv("BITEDGE_PRS", prs)
 
     from paper_1401_5245_b200 import cuda as cu
 
     rng = np.random.default_rng(G)
-    H, W = 301, 2048 + 96
+    H = 301
     a = (rng.random((H, W)) < 0.5).astype(np.uint8)
     whole = cu.pack_edges_u8(_t(a, cuda_dev), 1)
     pk = torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev)
