@@ -207,6 +207,21 @@ int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, 
                        uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,
                        void *stream1, int blocking);
 
+/* The drop-in host flow for ONE image in one call -- BitImage.from_array(a)
+ * (bitimage.py:122-136) + detect_edges_mask / edge_set
+ * + .words (bitimage.py:140-147): uint8 pixels [h][w] (nonzero = white) in
+ * page-locked host memory are copied to dev_pix (>= h*w bytes), packed and
+ * edge-detected in one kernel into dev_out (uint64 BitImage words
+ * [h][ceil(w/64)]; the packed input also into dev_packed when non-NULL), and the
+ * words are copied to host_out (page-locked, same shape).  With dev_pix and/or
+ * dev_out NULL the kernel reads the pixels / writes the words over PCIe itself
+ * (mapped page-locked memory; small images, w < 1024), which skips the copy
+ * operations' fixed latency.  Returns once the stream is idle: host_out is
+ * ready and every buffer may be reused. */
+int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_bit,
+                       int emit_edgeset, uint8_t *dev_pix_or_null, uint64_t *dev_packed_or_null,
+                       uint64_t *dev_out_or_null, uint64_t *host_out, void *stream);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);
 int be_abi_version(void);

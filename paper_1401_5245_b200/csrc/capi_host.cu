@@ -105,6 +105,42 @@ int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64
     return BE_OK;
 }
 
+int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_bit,
+                       int emit_edgeset, uint8_t *dev_pix_or_null, uint64_t *dev_packed_or_null,
+                       uint64_t *dev_out_or_null, uint64_t *host_out, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, 64, 1, h, w, fill_bit);
+    if (rc) return rc;
+    if (!host_pix || !host_out) return fail(BE_EINVAL, "host buffers must not be NULL");
+    const bool zc = dev_pix_or_null == nullptr || dev_out_or_null == nullptr;
+    if (zc && w >= 1024)
+        return fail(BE_EINVAL, "zero-copy host access (NULL dev_pix / dev_out) needs w < 1024");
+    const int64_t wp = G.wp / 2;                                 // uint64 words per row
+    cudaStream_t st = S(stream);
+    const uint8_t *src = host_pix;                               // zero-copy: read over PCIe
+    if (dev_pix_or_null) {
+        cudaError_t e = cudaMemcpyAsync(dev_pix_or_null, host_pix, (size_t)h * w,
+                                        cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
+        src = dev_pix_or_null;
+    }
+    uint64_t *dst = dev_out_or_null ? dev_out_or_null : host_out;   // zero-copy: write over PCIe
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    // one launch: pack (bitimage.py:122-136) + edges, uint64 words
+    rc = edges_impl(src, 1, w, nullptr, nullptr, emit_edgeset ? nullptr : (uint32_t *)dst,
+                    emit_edgeset ? (uint32_t *)dst : nullptr, side,
+                    (uint32_t *)dev_packed_or_null, 64, wp, 1, h, w, fill_bit, 0, h, st);
+    if (rc) return rc;
+    if (dev_out_or_null) {
+        cudaError_t e = cudaMemcpyAsync(host_out, dev_out_or_null, (size_t)h * wp * 8,
+                                        cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return fail((int)e, "D2H: %s", cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    return BE_OK;
+}
+
 int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
                        int64_t w, int fill_bit, int halo_flags, void *const dev_in[2],
                        uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,

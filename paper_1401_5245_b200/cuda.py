@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _capi
@@ -202,6 +204,51 @@ def pack_and_edges(pixels: torch.Tensor, border=WHITE_OUTSIDE, *, word_bits: int
     if rc:
         _capi.check(rc)
     return e, pk
+
+
+# zero-copy bound for host_detect: the kernel reads / writes host memory over
+# PCIe itself, which beats the copy operations' fixed latency for small images
+_ZERO_COPY_BYTES = 1 << 20
+
+
+def host_detect(host_pixels: torch.Tensor, border=WHITE_OUTSIDE, *, edgeset: bool = False,
+                device=None, zero_copy: bool | None = None):
+    """One host image through `be_host_detect_u64`: page-locked uint8 pixels
+    [H, W] (nonzero = white) -> (edges, packed, words): the edges as CUDA int64
+    BitImage words (None when the kernel wrote them straight to the host), the
+    packed input as CUDA int64 words, and the edges as a read-only host uint64
+    array -- from one call that uploads, packs + detects in one kernel,
+    downloads and waits (the drop-in's `detect_edges_mask(BitImage.from_array(a)).words`).
+    `zero_copy` (default: images up to 1 MiB, narrower than 1024 px): the kernel
+    reads the pixels and writes the words over PCIe itself, no copy operations."""
+    if host_pixels.is_cuda or not host_pixels.is_pinned() or host_pixels.dim() != 2 or \
+            host_pixels.dtype != torch.uint8 or not host_pixels.is_contiguous():
+        raise ValueError("host_pixels must be a contiguous page-locked uint8 [H, W] host tensor")
+    h, w = host_pixels.shape
+    if w < 1 or h < 1:
+        raise ValueError(f"image dimensions must be at least 1x1, got {w}x{h}")
+    if zero_copy is None:
+        zero_copy = h * w <= _ZERO_COPY_BYTES and w < 1024
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    wp = -(-w // 64)
+    packed = torch.empty((h, wp), dtype=torch.int64, device=dev)
+    host = torch.empty((h, wp), dtype=torch.int64, pin_memory=True)
+    if zero_copy:
+        dpix = out = None
+    else:
+        dpix = torch.empty((h, w), dtype=torch.uint8, device=dev)
+        out = torch.empty((h, wp), dtype=torch.int64, device=dev)
+    rc = _capi.fn("be_host_detect_u64")(host_pixels.data_ptr(), h, w, fill_bit(border),
+                                        1 if edgeset else 0,
+                                        None if dpix is None else dpix.data_ptr(), packed.data_ptr(),
+                                        None if out is None else out.data_ptr(), host.data_ptr(),
+                                        _stream(packed))
+    if rc:
+        _capi.check(rc)
+    words = host.numpy().view(np.uint64)
+    words.setflags(write=False)
+    return out, packed, words
 
 
 def _pixels(pixels: torch.Tensor, what="pixels"):

@@ -56,6 +56,15 @@ def fundamental_edge(img: BitImage, mask: BitImage, side: Direction,
 
 def _edges(img: BitImage, border: BorderPolicy, edgeset: bool) -> BitImage:
     pix = img._take_pixels()
+    if pix is not None and not pix.is_cuda:
+        # from_array of a host array, nothing uploaded yet: upload, pack + edges
+        # (one launch) and the result's download in one native call; the result
+        # holds its words on both sides, the input keeps its packed words in HBM
+        out, packed, host = _cuda().host_detect(pix, border.fill_bit, edgeset=edgeset)
+        img._adopt_packed(packed)
+        res = BitImage._wrap(img.width, img.height, out)   # out None: uploaded on demand
+        res._words = host
+        return res
     if pix is not None:
         # image from from_array, not packed yet: pack + edges in one launch
         out, packed = _cuda().pack_and_edges(pix, border.fill_bit, edgeset=edgeset)

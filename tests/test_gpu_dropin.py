@@ -167,3 +167,79 @@ def test_u8_to_u64_words(w, cuda_dev):
         expt = np.stack([P.from_array((x >= 200).astype(np.uint8)).words
                          for x in gray.cpu().numpy()])
         assert (th == expt).all(), (w, "threshold")
+
+
+@pytest.mark.parametrize("policy", ["WHITE_OUTSIDE", "BLACK_OUTSIDE"])
+def test_host_flow_one_call(policy, cuda_dev):
+    """from_array of a host array keeps a private page-locked copy; the first
+    detect_edges_mask / edge_set uploads, packs + detects and downloads in one
+    native call (be_host_detect_u64): host words ready, device words equal, the
+    input keeps its packed words, and later mutation of the caller's array does
+    not leak in."""
+    import torch
+
+    from paper_1401_5245_b200.bitimage import BitImage, BorderPolicy
+    from paper_1401_5245_b200.edge import detect_edges_mask, edge_set
+
+    b = BorderPolicy[policy]
+    for seed, (h, w) in enumerate([(1, 1), (256, 256), (37, 130), (3, 1100), (70, 4160),
+                                   (2, 3000), (500, 1)]):
+        a = _img(100 + seed, h, w)
+        ref = P.from_array(a)
+        exp = P.detect_edges_mask(ref, b.value).words
+        src = a.copy()
+        img = BitImage.from_array(src)
+        src[...] = 0                                        # the image owns its pixels
+        assert img._pix is not None and not img._pix[0].is_cuda
+        e = detect_edges_mask(img, b)
+        assert e._words is not None                         # downloaded by the same call
+        assert (e.words == exp).all()
+        assert (e.device_words().cpu().numpy().view(np.uint64) == exp).all()
+        assert (img.words == ref.words).all()               # packed input kept
+        # the result chains on the device like any other image
+        assert (detect_edges_mask(e, b).words ==
+                P.detect_edges_mask(P.make(w, h, exp.copy()), b.value).words).all()
+        es = edge_set(BitImage.from_array(a), b)
+        assert (es.words == P.edge_set(ref, b.value).words).all()
+    torch.cuda.synchronize()
+
+
+def test_host_flow_input_dtypes(cuda_dev):
+    """Nonzero = white for every input dtype (bitimage.py:124,133)."""
+    from paper_1401_5245_b200.bitimage import BitImage
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    rng = np.random.default_rng(7)
+    base = (rng.random((33, 77)) < 0.5)
+    exp = P.detect_edges_mask(P.from_array(base.astype(np.uint8))).words
+    for a in (base, base.astype(np.int8) * -3, base.astype(np.uint8) * 200,
+              base.astype(np.int32) * 5, base.astype(np.float32) * 0.5, base.astype(np.int64) - 0,
+              np.asfortranarray(base.astype(np.uint8)), base.astype(np.uint8)[:, ::-1][:, ::-1]):
+        assert (detect_edges_mask(BitImage.from_array(a)).words == exp).all(), a.dtype
+
+
+@pytest.mark.parametrize("zero_copy", [True, False])
+def test_host_detect_copy_modes(zero_copy, cuda_dev):
+    """be_host_detect_u64 with device staging (H2D / kernel / D2H) and with the
+    kernel reading and writing page-locked host memory itself: same words."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    for seed, (h, w) in enumerate([(1, 1), (64, 64), (256, 256), (9, 1000), (130, 63)]):
+        a = _img(200 + seed, h, w)
+        hp = torch.empty((h, w), dtype=torch.uint8, pin_memory=True)
+        hp.numpy()[...] = a
+        ref = P.from_array(a)
+        for fill in (1, 0):
+            for es in (False, True):
+                out, packed, words = cu.host_detect(hp, fill, edgeset=es, zero_copy=zero_copy)
+                exp = (P.edge_set if es else P.detect_edges_mask)(ref, fill).words
+                assert (words == exp).all(), (h, w, fill, es)
+                assert (packed.cpu().numpy().view(np.uint64) == ref.words).all()
+                if out is not None:
+                    assert (out.cpu().numpy().view(np.uint64) == exp).all()
+    if zero_copy:
+        hp = torch.empty((2, 1024), dtype=torch.uint8, pin_memory=True)
+        with pytest.raises(ValueError, match="zero-copy"):
+            cu.host_detect(hp, 1, zero_copy=True)
