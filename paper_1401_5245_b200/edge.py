@@ -56,29 +56,25 @@ def fundamental_edge(img: BitImage, mask: BitImage, side: Direction,
 
 def _edges(img: BitImage, border: BorderPolicy, edgeset: bool) -> BitImage:
     pix = img._take_pixels()
-    if pix is not None and not pix.is_cuda:
+    if pix is not None:
         # from_array of a host array, nothing uploaded yet: upload, pack + edges
         # (one launch) and the result's download in one native call; the result
-        # holds its words on both sides, the input keeps its packed words in HBM
+        # holds its words on the host (and in HBM when the call staged them
+        # there), the input keeps its packed words in HBM
         out, packed, host = _cuda().host_detect(pix, border.fill_bit, edgeset=edgeset)
         img._adopt_packed(packed)
         res = BitImage._wrap(img.width, img.height, out)   # out None: uploaded on demand
         res._words = host
         return res
-    if pix is not None:
-        # image from from_array, not packed yet: pack + edges in one launch
-        out, packed = _cuda().pack_and_edges(pix, border.fill_bit, edgeset=edgeset)
-        img._adopt_packed(packed)
-    else:
-        out = _cuda().edges_packed(img.device_words(), img.width, border.fill_bit,
-                                   edgeset=edgeset)
+    out = _cuda().edges_packed(img.device_words(), img.width, border.fill_bit, edgeset=edgeset)
     return BitImage._wrap(img.width, img.height, out)
 
 
 def detect_edges_mask(img: BitImage, border: BorderPolicy = _WHITE) -> BitImage:
     """invert(OR of the four fundamental EdgeSets): edge pixels black (0), all
     others white (1), padding 1.  One kernel launch -- which
-    also packs the image when it came from `from_array` and was not packed yet."""
+    also packs the image when it came from `from_array` of a host array and was
+    not packed yet (then upload, kernel and the result's download are one call)."""
     return _edges(img, border, False)
 
 

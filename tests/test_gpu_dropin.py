@@ -1,8 +1,8 @@
-"""The drop-in BitImage's deferred pack: `from_array` on a host array uploads
-the pixels and defers packing to the first consumer; detect_edges_mask /
-edge_set fuse it into their launch (and leave the packed words behind), every
-other consumer packs first.  All results word-identical to the reference
-composition (oracle/port.py)."""
+"""The drop-in BitImage's deferred pack: `from_array` on a host array keeps a
+page-locked copy of the pixels; detect_edges_mask / edge_set run upload, pack +
+edges and the result's download as one call (and leave the packed words
+behind), every other consumer uploads and packs first.  All results
+word-identical to the reference composition (oracle/port.py)."""
 
 import numpy as np
 import pytest
@@ -190,7 +190,7 @@ def test_host_flow_one_call(policy, cuda_dev):
         src = a.copy()
         img = BitImage.from_array(src)
         src[...] = 0                                        # the image owns its pixels
-        assert img._pix is not None and not img._pix[0].is_cuda
+        assert img._pix is not None and not img._pix.is_cuda
         e = detect_edges_mask(img, b)
         assert e._words is not None                         # downloaded by the same call
         assert (e.words == exp).all()
