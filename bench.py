@@ -605,6 +605,8 @@ def run_ours(args):
         e2e["pcie_h2d_gbs"] = round(h2d, 2)
         e2e["copies_only_gpx_s"] = round(px_e2e / (fl_ms / 1e3) / 1e9, 2)
         e2e["frac_of_copies_only"] = round(e2e["value"] / e2e["copies_only_gpx_s"], 3)
+        e2e["transfer"] = ("kernel reads / writes page-locked host memory (zero-copy)"
+                           if pipe.zero_copy else "copy engines, chunks on two streams")
 
     # ---- parity gate on the measured output (before reporting a number)
     parity = None

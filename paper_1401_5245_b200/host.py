@@ -27,10 +27,18 @@ class HostBatchEdges:
 
     def __init__(self, shape, kind: str = "u8", width: int | None = None, border=1,
                  chunk_images: int | None = None, device=None, chunk_rows: int | None = None,
-                 halo_rows: tuple = (False, False)):
+                 halo_rows: tuple = (False, False), zero_copy: bool | None = None):
         """`halo_rows=(above, below)`: the host input of a single-image row slab
         also holds the row above its first row / below its last row (a row shard
-        of a larger raster, multi-GPU); the result covers the slab's own rows."""
+        of a larger raster, multi-GPU); the result covers the slab's own rows.
+
+        `zero_copy` (default: batches of up to 4 MiB of input, uint8 rows
+        narrower than 1024 px): the kernel reads the page-locked host input and
+        writes the page-locked host output over PCIe itself -- no copy
+        operations, whose fixed latency dominates small batches (one 256^2 image:
+        7 us against 20 us staged; scripts/zero_copy_rate.py).  Larger batches
+        stream faster through the copy engines.  Buffers that are not
+        page-locked always take the staged path."""
         if kind not in ("u8", "packed"):
             raise ValueError("kind must be 'u8' or 'packed'")
         self.device = torch.device(device) if device is not None else torch.device(
@@ -78,6 +86,13 @@ class HostBatchEdges:
             self.d_out = [torch.empty((self.chunk,) + self.out_shape[1:], dtype=torch.int32,
                                       device=self.device) for _ in range(2)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(2)]
+        if zero_copy is None:
+            zero_copy = (not self.rows_mode and n * per_img <= (4 << 20) and
+                         (kind == "packed" or self.width < 1024))
+        elif zero_copy and (self.rows_mode or (kind == "u8" and self.width >= 1024)):
+            raise ValueError("zero_copy needs whole images and, for uint8, rows narrower "
+                             "than 1024 px (the wider kernels stage rows with TMA)")
+        self.zero_copy = bool(zero_copy)
         self.h2d_bytes = n * h * s * (1 if kind == "u8" else 4)
         if self.rows_mode:          # + the halo rows each chunk copies in
             chunks = -(-h // self.chunk)
@@ -106,6 +121,21 @@ class HostBatchEdges:
 
     def _run(self, host_in, host_out, blocking: bool) -> None:
         P = ctypes.c_void_p
+        if self.zero_copy and host_in.is_pinned() and host_out.is_pinned():
+            # one kernel over page-locked host memory (mapped: same address on the device)
+            st = self.streams[0]
+            wp = self.out_shape[2]
+            if self.kind == "u8":
+                _capi.call("be_pack_edge_u8", P(host_in.data_ptr()), P(host_out.data_ptr()),
+                           self.n, self.h, self.width, self.width, wp, cu.fill_bit(self.border),
+                           None, P(st.cuda_stream))
+            else:
+                _capi.call("be_edge_packed_u32", P(host_in.data_ptr()), P(host_out.data_ptr()),
+                           self.n, self.h, self.width, wp, cu.fill_bit(self.border), 0,
+                           P(st.cuda_stream))
+            if blocking:
+                st.synchronize()
+            return
         if self.rows_mode:
             _capi.call("be_host_edges_rows", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                        P(host_out.data_ptr()), self.h, self.width, cu.fill_bit(self.border),

@@ -411,26 +411,53 @@ def test_row_slabs_with_halos_equal_whole(cuda_dev, G, W, prs, monkeypatch):
         assert torch.equal(torch.cat(parts), whole), (G, fill)
 
 
-def test_host_pipeline_e2e(cuda_dev):
+@pytest.mark.parametrize("zc", [False, True, None])     # staged copies / kernel over host memory / auto
+def test_host_pipeline_e2e(cuda_dev, zc):
     from paper_1401_5245_b200 import synth
     from paper_1401_5245_b200.host import HostBatchEdges
 
     imgs = synth.c2_images(512)
-    pipe = HostBatchEdges(imgs.shape, kind="u8", chunk_images=100)
+    pipe = HostBatchEdges(imgs.shape, kind="u8", chunk_images=100, zero_copy=zc)
+    assert pipe.zero_copy == (zc is not False)
     hin, hout = pipe.new_host_buffers()
     hin.copy_(imgs)
     pipe(hin, hout)
     assert (hout.numpy().view(np.uint32) == cscan.scan_u8(imgs.numpy(), 1)).all()
     c3 = synth.c3_words(h=512)
-    pipe2 = HostBatchEdges((1, 512, 256), kind="packed", width=8192, chunk_images=1)
+    pipe2 = HostBatchEdges((1, 512, 256), kind="packed", width=8192, chunk_images=1, zero_copy=zc)
     import torch
 
     hin2 = torch.from_numpy(c3.view(np.int32)).reshape(1, 512, 256).pin_memory()
     out2 = pipe2(hin2)
     assert (out2.numpy().view(np.uint32)[0] == cscan.scan_p32(c3, 8192)).all()
+    # pageable buffers always take the staged path (the kernel cannot map them)
+    out3 = torch.empty(pipe.out_shape, dtype=torch.int32)
+    pipe(imgs.clone(), out3)
+    assert (out3.numpy().view(np.uint32) == cscan.scan_u8(imgs.numpy(), 1)).all()
+    # ragged uint8 rows and a single C1-sized image, both border fills
+    rng = np.random.default_rng(5)
+    for (n, h, w) in ((1, 256, 256), (3, 37, 130), (1, 1, 1)):
+        a = (rng.random((n, h, w)) < 0.5).astype(np.uint8) * 7
+        for fill in (1, 0):
+            p3 = HostBatchEdges((n, h, w), kind="u8", border=fill, zero_copy=zc)
+            hi, ho = p3.new_host_buffers()
+            hi.copy_(torch.from_numpy(a))
+            got = p3.submit(hi, ho).synchronize().numpy().view(np.uint32)
+            assert (got == cscan.scan_u8(a, fill)).all(), (n, h, w, fill, zc)
 
 
-def test_host_pipeline_submit(cuda_dev):
+def test_host_pipeline_zero_copy_limits(cuda_dev):
+    from paper_1401_5245_b200.host import HostBatchEdges
+
+    assert not HostBatchEdges((4096, 64, 64), kind="u8").zero_copy          # 16 MiB: copy engines
+    assert HostBatchEdges((1, 256, 256), kind="u8").zero_copy
+    assert not HostBatchEdges((1, 64, 1024), kind="u8").zero_copy            # TMA kernels
+    with pytest.raises(ValueError, match="zero_copy"):
+        HostBatchEdges((1, 64, 2048), kind="u8", zero_copy=True)
+
+
+@pytest.mark.parametrize("zc", [False, None])
+def test_host_pipeline_submit(cuda_dev, zc):
     """HostBatchEdges.submit: several batches in flight over two host output
     buffers (the bench's e2e loop), each result exact when its handle syncs."""
     import torch
@@ -439,7 +466,7 @@ def test_host_pipeline_submit(cuda_dev):
     from paper_1401_5245_b200.host import HostBatchEdges
 
     batches = [synth.c2_images(300, start=300 * k) for k in range(3)]   # distinct images
-    pipe = HostBatchEdges(tuple(batches[0].shape), kind="u8", chunk_images=64)
+    pipe = HostBatchEdges(tuple(batches[0].shape), kind="u8", chunk_images=64, zero_copy=zc)
     hins = [torch.empty(tuple(b.shape), dtype=torch.uint8, pin_memory=True) for b in batches]
     for h_, b in zip(hins, batches):
         h_.copy_(b)
