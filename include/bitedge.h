@@ -161,11 +161,14 @@ int be_p4_decode(const uint8_t *p4, void *out, int word_bits, int64_t n, int64_t
                  int64_t out_row_stride_words, void *stream);
 int be_p4_encode(const void *in, uint8_t *p4, int word_bits, int64_t n, int64_t h, int64_t w,
                  int64_t in_row_stride_words, void *stream);
-/* detect_edges_mask from a P4 payload to a P4 payload.  When a P4 row is a whole
- * number of 16-byte chunks (w % 128 in 121..128 or 0) kernel K1 reads and writes
- * P4 directly (kept in the P4 byte order; only the centre row is byte-swapped for
- * the horizontal shifts, 0.25 B/px); otherwise it runs decode -> K1 -> encode
- * through `scratch_or_null` (2 * n * h * ceil(w/32) words). */
+/* detect_edges_mask from a P4 payload to a P4 payload, one kernel for every
+ * width.  When a P4 row is a whole number of 16-byte chunks (w % 128 in
+ * 121..128 or 0) kernel K1 reads and writes P4 directly (kept in the P4 byte
+ * order; only the centre row is byte-swapped for the horizontal shifts,
+ * 0.25 B/px); other rows start at any byte and a byte-granular kernel does the
+ * same in one pass.  `scratch_or_null` (2 * n * h * ceil(w/32) words) is only
+ * used with BITEDGE_P4_UNFUSED set: decode -> K1 -> encode, the reference path
+ * the tests compare against. */
 int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int64_t h, int64_t w,
                 int fill_bit, uint32_t *scratch_or_null, void *stream);
 

@@ -45,6 +45,103 @@ __global__ void p4_encode_kernel(const uint32_t *__restrict__ in, uint8_t *__res
     }
 }
 
+// P4 payloads of ANY width in one pass (F1 for rows that are not 16-byte
+// multiples, e.g. the CLI's arbitrary PBM files): rows are ceil(w/8) bytes
+// packed back to back, so a row starts at any byte.  Thread = one 32-pixel word
+// of one row: it reads its (up to) 4 bytes of the row above, the row and the
+// row below, plus the byte either side of its centre bytes for the horizontal
+// neighbours -- byte loads, L1-cached, shared by the neighbouring threads --
+// evaluates the edge formula in the white domain (exactly K1's, with the fill at
+// pixel 0, pixel w-1 and every image's first / last row) and stores its bytes
+// (P4 polarity, padding bits 0 as the encoder writes them).
+__device__ __forceinline__ uint32_t p4_ld8(const uint8_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t p4_ld32(const uint8_t *p) {
+    return __ldg(reinterpret_cast<const uint32_t *>(p));
+}
+
+// Little-endian 4 bytes of the payload at byte offset `off` (bytes at or past
+// `total` read as 0).  With a 4-byte aligned payload: two aligned loads and a
+// funnel shift; at the very end of the buffer, or for an unaligned payload,
+// byte loads (never a byte outside [0, total)).
+__device__ __forceinline__ uint32_t p4_get4(const uint8_t *in, int64_t off, int64_t total,
+                                            bool al) {
+    const int64_t a = off & ~(int64_t)3;
+    if (al && a + 8 <= total)
+        return __funnelshift_r(p4_ld32(in + a), p4_ld32(in + a + 4), (uint32_t)(off & 3) * 8);
+    uint32_t v = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (off + k < total) v |= p4_ld8(in + off + k) << (8 * k);
+    return v;
+}
+
+// Thread = one 32-pixel word column of a strip of R rows (rows walked with the
+// up / centre / down words rolling in registers: one new row of 4 bytes per
+// output row, plus the byte either side of the centre word for the horizontal
+// neighbours), so the per-thread setup is paid once per R words.
+template <int R>
+__global__ void __launch_bounds__(256)
+p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, WordGeom g,
+                      int64_t rb, uint32_t nstrips, FastDiv dv_wp, FastDiv dv_h) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;    // < 2^32 (host check)
+    const uint32_t strip = fdiv(t, dv_wp);
+    if (strip >= nstrips) return;
+    const int pw = (int)(t - strip * (uint32_t)g.wp);
+    const int64_t nbytes = g.nrows * rb;
+    const uint32_t fw = g.fillword;
+    const bool al = ((uintptr_t)in & 3) == 0;
+    const int64_t b0 = 4 * (int64_t)pw;
+    const int nb = rb - b0 < 4 ? (int)(rb - b0) : 4;
+    // bytes past the row (the next row's) read as black in P4 = white here:
+    // they are padding positions, forced below
+    const uint32_t keep = nb == 4 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (8 * nb));
+    const bool tail = pw == g.pl, has_r = b0 + 4 < rb;
+    const uint32_t r0 = strip * R;                               // < 2^32 (host check)
+    uint32_t y = r0 - fdiv(r0, dv_h) * (uint32_t)g.h;
+    int64_t off = (int64_t)r0 * rb + b0;
+    // white-domain, pixel-order word of the 4 bytes at byte offset o
+    auto word = [&](int64_t o) {
+        return ~(__byte_perm(p4_get4(in, o, nbytes, al), 0, 0x0123) & keep);
+    };
+    uint32_t up = y == 0 ? fw : word(off - rb);
+    uint32_t c = word(off);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (r0 + i >= g.nrows) break;
+        const bool last = y == (uint32_t)g.h - 1;
+        const uint32_t nx = r0 + i + 1 < g.nrows ? word(off + rb) : fw;
+        const uint32_t d = last ? fw : nx;
+        // its bit 0: pixel 32*pw - 1 (last bit of the byte before); bit 31: pixel 32*pw + 32
+        const uint32_t lw = pw > 0 ? ~p4_ld8(in + off - 1) : fw;
+        const uint32_t rw = has_r ? ~(p4_ld8(in + off + 4) << 24) : fw;
+        const uint32_t ln = __funnelshift_r(c, lw, 1);
+        uint32_t rn = __funnelshift_l(rw, c, 1);
+        uint32_t f = 0u;
+        if (tail) {                               // pixel w-1 reads the fill; padding -> 1
+            rn = (rn & ~g.lastbit) | (fw & g.lastbit);
+            f = g.padmask;
+        }
+        const uint32_t e = ~(c | ~(ln | rn | up | d) | f);   // P4: 1 = black edge pixel
+        uint8_t *o = out + off;
+        if (nb == 4 && ((uintptr_t)o & 3) == 0) {
+            *reinterpret_cast<uint32_t *>(o) = __byte_perm(e, 0, 0x0123);   // bytes in P4 order
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < nb) o[k] = (uint8_t)(e >> (24 - 8 * k));
+        }
+        up = last ? fw : c;                       // the next row starts a new image after `last`
+        c = nx;
+        y = last ? 0u : y + 1;
+        off += rb;
+    }
+}
+
 }  // namespace capi
 }  // namespace bitedge
 
@@ -138,7 +235,20 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }
-    // general path: decode -> K1 -> encode through caller scratch (2 word rasters)
+    // any other row length: the byte-granular single-pass kernel
+    constexpr int kR = 8;
+    const int64_t nstrips = (n * h + kR - 1) / kR;
+    const bool fits = nstrips * G.wp + 256 < ((int64_t)1 << 32) && n * h < ((int64_t)1 << 32) - kR;
+    if (!getenv("BITEDGE_P4_UNFUSED") && fits) {
+        WordGeom g = word_geom(G, G.wp);
+        const int64_t threads = nstrips * g.wp;
+        p4_edges_bytes_kernel<kR><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+            p4_in, p4_out, g, rb, (uint32_t)nstrips, make_fastdiv((uint32_t)g.wp),
+            make_fastdiv((uint32_t)g.h));
+        return cuda_check("p4_edges_bytes_kernel");
+    }
+    // reference path (BITEDGE_P4_UNFUSED, or > 2^32 threads): decode -> K1 ->
+    // encode through caller scratch (2 word rasters)
     if (scratch_or_null == nullptr)
         return fail(BE_EINVAL, "unaligned P4 rows (ceil(w/8) %% 16 != 0) need a scratch buffer of "
                                "2 * n * h * ceil(w/32) words");

@@ -87,7 +87,7 @@ def test_fuzz_p4(seed, cuda_dev):
         fill = int(rng.integers(0, 2))
         a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
         rb = (w + 7) // 8
-        bits = np.ones((n, h, rb * 8), np.uint8)
+        bits = rng.integers(0, 2, (n, h, rb * 8)).astype(np.uint8)   # garbage padding bits
         bits[..., :w] = a
         payload = np.packbits(1 - bits, axis=-1)                     # P4: 1 = black
         out = pbm.detect_p4(torch.from_numpy(payload.reshape(-1).copy()).to(cuda_dev), n, h, w,
