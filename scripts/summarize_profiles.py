@@ -111,7 +111,10 @@ def main():
              "Captured by `scripts/gpu_profiles.sh` on one B200 (`ncu --set full --clock-control none`,",
              "default cache control = flushed between replays, so durations are cold-cache and",
              "serialised); summarised by `scripts/summarize_profiles.py`.  Bench numbers are NOT",
-             "taken under ncu.", "",
+             "taken under ncu.  DRAM writes of the small outputs (C1-C3: 8 KB - 8 MiB) read",
+             "~0 per launch: the write-back L2 (126 MB) still holds them when the replay's",
+             "counters stop, and they reach DRAM only on eviction; the bench's rotating",
+             "buffer pools (> 3x L2) make every step pay that write-back eventually.", "",
              f"## Launch list of `python bench.py --config c2 --steps 200 --warmup 5 --no-cpu` ({nl} launches)",
              "", "| kernel | share of GPU time |", "|---|---|"]
     lines += [f"| `{k}` | {v:.1%} |" for k, v in shares]
