@@ -243,3 +243,18 @@ def test_host_detect_copy_modes(zero_copy, cuda_dev):
         hp = torch.empty((2, 1024), dtype=torch.uint8, pin_memory=True)
         with pytest.raises(ValueError, match="zero-copy"):
             cu.host_detect(hp, 1, zero_copy=True)
+
+
+def test_large_host_array_packed_at_once(cuda_dev, monkeypatch):
+    """Above the page-locked copy limit from_array uploads and packs at once
+    (same words, same edges)."""
+    from paper_1401_5245_b200 import bitimage as B
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    monkeypatch.setattr(B, "_PINNED_MAX", 1000)
+    for a in (_img(7, 40, 130), _img(8, 40, 130).astype(np.int32)):
+        img = B.BitImage.from_array(a)
+        assert img._pix is None and img._dev is not None
+        ref = P.from_array(a)
+        assert (img.words == ref.words).all()
+        assert (detect_edges_mask(img).words == P.detect_edges_mask(ref).words).all()
