@@ -64,7 +64,7 @@ inline int make_geometry(Geometry &G, int word_bits, int64_t n, int64_t h, int64
                     (long long)w, (long long)h);
     if (fill_bit != 0 && fill_bit != 1)
         return fail(BE_EINVAL, "fill_bit must be 0 or 1, got %d", fill_bit);
-    if (w > (int64_t)1 << 36 || n * h > ((int64_t)1 << 40))
+    if (w > (int64_t)1 << 36 || h > ((int64_t)1 << 40) || (n > 0 && h > ((int64_t)1 << 40) / n))
         return fail(BE_EINVAL, "raster too large");
     G.n = n; G.h = h; G.w = w; G.word_bits = word_bits;
     const int64_t wp = word_bits == 64 ? 2 * ((w + 63) / 64) : (w + 31) / 32;

@@ -37,6 +37,8 @@ def test_library_is_sm100a():
     ((None, None, 1, 5, 5, 1, 2, 0, None), "fill_bit"),
     ((ctypes.c_void_p(16), ctypes.c_void_p(32), 1, 5, 100, 1, 1, 0, None), "row stride"),
     ((None, None, 1, 5, 5, 1, 1, 0, None), "NULL"),
+    ((None, None, 1 << 40, 1 << 40, 5, 1, 1, 0, None), "too large"),   # n * h would overflow
+    ((None, None, 1, 5, 1 << 40, 1 << 35, 1, 0, None), "too large"),
 ])
 def test_abi_validation_errors(args, msg):
     """Invalid arguments fail before any launch with a negative code -> ValueError."""
