@@ -115,6 +115,20 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
     const bool zc = dev_pix_or_null == nullptr || dev_out_or_null == nullptr;
     if (zc && w >= 1024)
         return fail(BE_EINVAL, "zero-copy host access (NULL dev_pix / dev_out) needs w < 1024");
+    // the kernel may only touch page-locked (mapped) host memory: refuse anything
+    // else here rather than fault on the device
+    auto pinned = [](const void *p) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    if (!dev_pix_or_null && !pinned(host_pix))
+        return fail(BE_EINVAL, "zero-copy input must be page-locked host memory");
+    if (!dev_out_or_null && !pinned(host_out))
+        return fail(BE_EINVAL, "zero-copy output must be page-locked host memory");
     const int64_t wp = G.wp / 2;                                 // uint64 words per row
     cudaStream_t st = S(stream);
     const uint8_t *src = host_pix;                               // zero-copy: read over PCIe

@@ -258,3 +258,24 @@ def test_large_host_array_packed_at_once(cuda_dev, monkeypatch):
         ref = P.from_array(a)
         assert (img.words == ref.words).all()
         assert (detect_edges_mask(img).words == P.detect_edges_mask(ref).words).all()
+
+
+def test_host_detect_refuses_pageable_zero_copy(cuda_dev):
+    """be_host_detect_u64's zero-copy mode checks that both host buffers are
+    page-locked instead of letting the kernel fault."""
+    import torch
+
+    from paper_1401_5245_b200 import _capi
+
+    h, w = 8, 40
+    pix = np.ones((h, w), np.uint8)                      # pageable
+    out = np.empty((h, 1), np.uint64)
+    pk = torch.empty((h, 1), dtype=torch.int64, device=cuda_dev)
+    rc = _capi.fn("be_host_detect_u64")(pix.ctypes.data, h, w, 1, 0, None, pk.data_ptr(), None,
+                                        out.ctypes.data, None)
+    assert rc < 0 and b"page-locked" in _capi.load().be_last_error()
+    torch.cuda.synchronize()                             # the context is still healthy
+    hp = torch.ones((h, w), dtype=torch.uint8, pin_memory=True)
+    rc = _capi.fn("be_host_detect_u64")(hp.data_ptr(), h, w, 1, 0, None, pk.data_ptr(), None,
+                                        out.ctypes.data, None)
+    assert rc < 0
