@@ -235,6 +235,36 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }
+    // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items
+    // loaded word by word
+    if (rb % 4 == 0 && al(p4_in, 4) && al(p4_out, 4) && !getenv("BITEDGE_P4_UNFUSED") &&
+        !getenv("BITEDGE_P4_BYTES") && n * h < ((int64_t)1 << 31)) {
+        RegParams rp;
+        memset(&rp, 0, sizeof(rp));
+        rp.in = (const char *)p4_in; rp.in_row_bytes = rb;
+        rp.in_end = (const char *)p4_in + n * h * rb;
+        rp.o_edges = (uint32_t *)p4_out; rp.out_stride = rb / 4;
+        rp.nrows = n * h; rp.row_lo = 0; rp.row_hi = n * h;
+        rp.h = (uint32_t)h; rp.w = w; rp.wp = G.wp; rp.pl = G.pl;
+        rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
+        rp.thr = 1;
+        rp.items = (G.wp + 3) / 4;
+        rp.vst = 0;                                  // rows are 4-byte aligned: word stores
+        const bool big = ((n * h + 3) / 4) * rp.items >= (int64_t)sm_count() * 4096 * 2;
+        const int rs = big ? 4 : 2;
+        rp.nstrips = (n * h + rs - 1) / rs;
+        const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
+        K1Div dv;
+        if (grid <= 0x7FFFFFFFLL && k1_setup(rp, dv)) {
+            if (rs == 4)
+                launch_k(edge_reg_packed_kernel<0, 4, 4, kOutEdges, false, true, false, true>,
+                         (unsigned)grid, 0, st, rp, dv);
+            else
+                launch_k(edge_reg_packed_kernel<0, 2, 4, kOutEdges, false, true, false, true>,
+                         (unsigned)grid, 0, st, rp, dv);
+            return cuda_check("edge_reg_packed_kernel<P4, word loads>");
+        }
+    }
     // any other row length: the byte-granular single-pass kernel
     constexpr int kR = 8;
     const int64_t nstrips = (n * h + kR - 1) / kR;

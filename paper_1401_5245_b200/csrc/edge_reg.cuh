@@ -51,6 +51,7 @@ struct RegParams {
     uint32_t *o_packed;      // kOutAll only: the packed input, padding 1 (or nullptr)
     int pdl_late;            // K2w: signal dependents after the stores, not at entry
     int oswap;               // K2t2: 1 = uint64 output words (pixel word p at uint32 index p ^ 1)
+    const char *in_end;      // K1 LD4: end of the input buffer (word loads stop there)
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -82,10 +83,12 @@ __device__ __forceinline__ void fix_tail(int pw, const RegParams &p, uint32_t &r
 
 // ---------------------------------------------------------------- K1: packed words
 
-// Load CW (4 or 8) consecutive uint32 words with one 128/256-bit load.
+// Load CW (8, 4 or 1) consecutive uint32 words with one 256/128/32-bit load.
 template <int CW>
 __device__ __forceinline__ void load_chunk(const char *p, uint32_t (&v)[CW]) {
-    if (CW == 8) {
+    if constexpr (CW == 1) {
+        v[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+    } else if constexpr (CW == 8) {
         asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
                        "=r"(v[6]), "=r"(v[7])
@@ -98,7 +101,9 @@ __device__ __forceinline__ void load_chunk(const char *p, uint32_t (&v)[CW]) {
 
 template <int CW>
 __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]) {
-    if (CW == 8) {
+    if constexpr (CW == 1) {
+        __stcs(p, v[0]);
+    } else if constexpr (CW == 8) {
         asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
                      "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                      : "memory");
@@ -152,7 +157,11 @@ inline bool k1_setup(const RegParams &p, K1Div &d) {
 // whole, there are no padding bits and the only border work at the right edge
 // is the fill word to the right of a row's last item, so the per-word tail
 // test (pixel w-1 fill, padding force) is compiled out.
-template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false>
+// LD4: rows are only 4-byte aligned (P4 payloads of w % 32 == 0 or 25..31): the
+// CW words of an item are loaded one by one, and a row's last item may run into
+// the next row (those words are padding positions) but never past `in_end`.
+template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false,
+          bool LD4 = false>
 __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
 edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
     pdl_wait();
@@ -186,7 +195,13 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
             if (i == 0 && gi < 0 && p.above) ptr = p.above + 4 * pw0;
             if (i >= 1 && gi == p.nrows && p.below) ptr = p.below + 4 * pw0;   // partial last strip too
         }
-        load_chunk<CW>(ptr, v[i]);                   // P4: raw bytes, converted per use
+        if constexpr (LD4) {
+#pragma unroll
+            for (int q = 0; q < CW; ++q)
+                v[i][q] = ptr + 4 * q + 4 <= p.in_end ? __ldg((const uint32_t *)ptr + q) : 0u;
+        } else {
+            load_chunk<CW>(ptr, v[i]);               // P4: raw bytes, converted per use
+        }
         if (i >= 1 && i <= RS) {
             // P4: raw bytes, byte-swapped at use (converting here would make the
             // warp wait for this load before issuing the next rows' loads); the

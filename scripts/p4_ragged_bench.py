@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1401_5245_b200 import pbm  # noqa: E402
 
 dev = torch.device("cuda:0")
-for (h, w) in ((8000, 8000), (2000, 2000), (256, 250)):
+for (h, w) in ((8000, 8000), (8000, 7993), (2000, 2000), (256, 250)):
     rb = (w + 7) // 8
     nbytes = h * rb
     pool = max(2, min(32, (3 * 126 << 20) // (2 * nbytes) + 1))

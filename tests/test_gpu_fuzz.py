@@ -73,17 +73,21 @@ def test_fuzz(seed, cuda_dev, monkeypatch):
             monkeypatch.delenv(k, raising=False)
 
 
+@pytest.mark.parametrize("knob", [None, "BITEDGE_P4_BYTES", "BITEDGE_P4_UNFUSED"])
 @pytest.mark.parametrize("seed", range(4))
-def test_fuzz_p4(seed, cuda_dev):
+def test_fuzz_p4(seed, knob, cuda_dev, monkeypatch):
     import torch
 
     from paper_1401_5245_b200 import pbm
 
+    if knob:
+        monkeypatch.setenv(knob, "1")
     rng = np.random.default_rng(2000 + seed)
     for _ in range(8):
         n = int(rng.integers(1, 4))
         h = int(rng.integers(1, 50))
-        w = int(rng.choice([int(rng.integers(1, 300)), 128, 1024, 2040, 4096]))
+        w = int(rng.choice([int(rng.integers(1, 300)), 128, 1024, 2040, 4096, 96, 8000,
+                            32 * int(rng.integers(1, 40)) - int(rng.integers(0, 8))]))
         fill = int(rng.integers(0, 2))
         a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
         rb = (w + 7) // 8
@@ -97,7 +101,6 @@ def test_fuzz_p4(seed, cuda_dev):
         assert (got == exp).all(), (n, h, w, fill)
         if w % 8:
             assert not (out[..., -1] & ((1 << (8 - w % 8)) - 1)).any()
-        os.environ.pop("BITEDGE_P4_UNFUSED", None)
 
 
 @pytest.mark.parametrize("knob", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")

@@ -594,7 +594,8 @@ def test_pbm_roundtrip_and_detect(cuda_dev):
     from paper_1401_5245_b200.pbm import detect_pbm, read_pbm, write_pbm
 
     rng = np.random.default_rng(4)
-    for (h, w) in [(5, 3), (17, 100), (9, 128), (33, 1024), (3, 250), (64, 2048), (2, 8192), (7, 1)]:
+    for (h, w) in [(5, 3), (17, 100), (9, 128), (33, 1024), (3, 250), (64, 2048), (2, 8192), (7, 1),
+                   (40, 96), (11, 8000), (6, 7993), (300, 32)]:
         a = (rng.random((h, w)) < 0.5).astype(np.uint8)
         img = BitImage.from_array(a)
         for raw in (True, False):
@@ -602,16 +603,19 @@ def test_pbm_roundtrip_and_detect(cuda_dev):
             assert read_pbm(data) == img, (h, w, raw)
         p4 = write_pbm(img, True)
         exp = P.to_array(P.detect_edges_mask(P.from_array(a), 1))
-        for unfused in (False, True):
-            import os
+        import os
 
-            if unfused:
-                os.environ["BITEDGE_P4_UNFUSED"] = "1"
+        # default dispatch (K1 on 16-byte or 4-byte rows, else the byte kernel),
+        # the byte kernel forced, and decode -> K1 -> encode
+        for knob in (None, "BITEDGE_P4_BYTES", "BITEDGE_P4_UNFUSED"):
+            if knob:
+                os.environ[knob] = "1"
             try:
                 got = read_pbm(detect_pbm(p4)).to_array()
             finally:
-                os.environ.pop("BITEDGE_P4_UNFUSED", None)
-            assert (got == exp).all(), (h, w, unfused)
+                if knob:
+                    os.environ.pop(knob, None)
+            assert (got == exp).all(), (h, w, knob)
         # P4 padding bits of the output are zero
         if w % 8:
             out = detect_pbm(p4)
