@@ -142,9 +142,9 @@ def test_input_garbage_does_not_leak(knob, cuda_dev, monkeypatch):
 
 
 @pytest.mark.parametrize("G", [256, 259], ids=["aligned", "misaligned"])
-@pytest.mark.parametrize("w", [128, 2048, 4096, 100, 1000, 7])
+@pytest.mark.parametrize("w", [128, 2048, 4096, 96, 8000, 32, 100, 1000, 7])
 def test_p4_guards(w, G, cuda_dev):
-    """be_p4_edges (fused K1 for 16-byte rows, decode -> K1 -> encode otherwise)
+    """be_p4_edges (K1 for 16-byte or 4-byte rows, the byte kernel otherwise)
     writes exactly n*h*ceil(w/8) bytes; the payload's unused trailing bits are
     zero (PBM convention)."""
     import ctypes
