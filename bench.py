@@ -220,6 +220,21 @@ def _units(kind, data, chunks):
     return "packed", parts
 
 
+def host_info():
+    """The host the CPU legs ran on (core counts and CPU model)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"cpu_count": os.cpu_count(), "affinity": aff, "model": model}
+
+
 def cpu_time_port(cfg, budget_s=3.0, reps_min=3):
     """cpu_baseline: the oracle port, single thread, median of >= 3 reps."""
     global _WORK
@@ -238,7 +253,8 @@ def cpu_time_port(cfg, budget_s=3.0, reps_min=3):
     med = statistics.median(times)
     return {"value": px / med / 1e9, "unit": "Gpixel/s", "cores": 1, "kind": "port",
             "sample": f"{cfg}: {px} px ({units} unit(s)) per rep, median of {len(times)} reps, "
-                      "oracle/port.py (reference BitImage composition, numpy, 1 thread)"}
+                      "oracle/port.py (reference BitImage composition, numpy, 1 thread)",
+            "host": host_info()}
 
 
 def run_reference(args):
@@ -283,7 +299,8 @@ def run_reference(args):
                    "step_sample_px": int(px_step)},
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": cores, "kind": "port",
                          "sample": f"{k} of {units} units ({int(px_step)} px) per step; "
-                                   "oracle/port.py = the reference BitImage composition"},
+                                   "oracle/port.py = the reference BitImage composition",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -29,6 +29,7 @@ def test_reference_arm_line():
     assert d["higher_is_better"] is True and d["config"]["workload"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
+    assert cb["host"]["cpu_count"] >= cb["cores"]
     assert d["e2e"] == {"value": d["value"], "unit": "Gpixel/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
 
