@@ -271,6 +271,18 @@ def run_reference(args):
     _WORK = _units(kind, data, cores)
     units = len(_WORK[1])
     px_per_unit = px_total / units
+    if units < 2:
+        # one indivisible unit (C1's single image): a process pool only adds
+        # its dispatch latency -- time it in this process, one core
+        cores = 1
+        for _ in range(args.warmup):
+            _cpu_unit(0)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _cpu_unit(0)
+        dt = time.perf_counter() - t0
+        k = 1
+        return _print_reference(args, cfg, px_per_unit * k, dt, cores, k, units)
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         # calibrate: seconds per unit on this pool
@@ -288,7 +300,10 @@ def run_reference(args):
         for _ in range(args.steps):
             pool.map(_cpu_unit, sel, chunksize=max(1, k // (4 * cores)))
         dt = time.perf_counter() - t0
-    px_step = px_per_unit * k
+    return _print_reference(args, cfg, px_per_unit * k, dt, cores, k, units)
+
+
+def _print_reference(args, cfg, px_step, dt, cores, k, units):
     value = px_step * args.steps / dt / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel/s", "impl": "reference",
