@@ -64,6 +64,12 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 
 // ---------------------------------------------------------------- register-direct kernel
 
+// K1's tail-free (ALIGNED) instantiations apply: edges only, 8-word items, whole
+// items with no padding bits (BITEDGE_K1_GENERIC turns them off).
+inline bool k1_aligned(bool edges_only, int cw, int64_t w) {
+    return edges_only && cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
+}
+
 // Launch helpers: dispatch the runtime choices onto template parameters.
 template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
@@ -75,10 +81,14 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cu
         else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         (void)cw;
     } else {
-        // whole 8-word items with no padding (w % 256 == 0: C3, C4): the tail-free kernels
-        const bool aligned = OUT == kOutEdges && !swap && cw == 8 && rp.w % 256 == 0 &&
-                             !getenv("BITEDGE_K1_GENERIC");
-        if (aligned && rs == 2) {
+        // whole 8-word items with no padding (w % 256 == 0: C3, C4, and the drop-in's
+        // uint64 BitImage words at those widths): the tail-free kernels
+        const bool aligned = k1_aligned(OUT == kOutEdges, cw, rp.w);
+        if (aligned && swap && rs == 2) {
+            launch_k(edge_reg_packed_kernel<1, 2, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
+        } else if (aligned && swap && rs == 4) {
+            launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
+        } else if (aligned && rs == 2) {
             launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
         } else if (aligned && rs == 4) {
             launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
@@ -201,7 +211,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
     const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
     int cw = (input_kind == 0 && in32 && !multi && !getenv("BITEDGE_CW4")) ? 8 : 4;
-    const int packed_rs = (input_kind == 0 && !G.swap && !big) ? 2 : 4;
+    // (uint64 words take 2-row strips only in the tail-free kernels)
+    const bool swap2 = !G.swap || k1_aligned(o_edges && !o_eset && !multi, cw, G.w);
+    const int packed_rs = (input_kind == 0 && swap2 && !big) ? 2 : 4;
     if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
