@@ -75,6 +75,17 @@ template <int OUT, bool HALO>
 int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cudaStream_t st) {
     K1Div dv;
     if (!k1_setup(rp, dv)) return kNoKernel;   // > 2^32 threads or rows: tile kernel
+    if (rp.in_end != nullptr) {                // UNAL: 4-byte aligned rows, 4-word items
+        if constexpr (OUT == kOutAll || HALO) {
+            return kNoKernel;
+        } else {
+            if (swap && rs == 2) launch_k(edge_reg_packed_kernel<1, 2, 4, OUT, false, false, false, true>, grid, 0, st, rp, dv);
+            else if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, false, false, false, true>, grid, 0, st, rp, dv);
+            else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, false, false, false, true>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<0, 4, 4, OUT, false, false, false, true>, grid, 0, st, rp, dv);
+            return cuda_check("edge_reg_packed_kernel<UNAL>");
+        }
+    }
     if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
         if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp, dv);
@@ -182,7 +193,13 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const char *e = getenv("BITEDGE_KERNEL");
     if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return kNoKernel;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
-    if (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0) return kNoKernel;
+    // packed rows that are only 4-byte aligned (not 16-byte multiples, or a
+    // strided view): K1's UNAL items, without halos
+    const bool unal = input_kind == 0 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
+                      !below && ((uintptr_t)in % 4) == 0 && in_row_bytes % 4 == 0 &&
+                      !getenv("BITEDGE_NO_UNAL");
+    if (!unal && (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0))
+        return kNoKernel;
     if (G.h >= ((int64_t)1 << 31)) return kNoKernel;
     RegParams rp;
     memset(&rp, 0, sizeof(rp));
@@ -211,8 +228,12 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
     const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
     int cw = (input_kind == 0 && in32 && !multi && !getenv("BITEDGE_CW4")) ? 8 : 4;
-    // (uint64 words take 2-row strips only in the tail-free kernels)
-    const bool swap2 = !G.swap || k1_aligned(o_edges && !o_eset && !multi, cw, G.w);
+    if (unal) {
+        if (multi) return kNoKernel;
+        rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + (int64_t)G.wp * 4;
+    }
+    // (uint64 words take 2-row strips only in the tail-free and UNAL kernels)
+    const bool swap2 = !G.swap || unal || k1_aligned(o_edges && !o_eset && !multi, cw, G.w);
     const int packed_rs = (input_kind == 0 && swap2 && !big) ? 2 : 4;
     if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
@@ -353,7 +374,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         const char *rse = getenv("BITEDGE_PRS");      // packed strip height experiments: 2/4/8
         if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
     }
-    if (multi && rs == 8) rs = 4;                    // kOutAll has 2- and 4-row strips
+    if ((multi || rp.in_end) && rs == 8) rs = 4;     // kOutAll / UNAL: 2- and 4-row strips
+    if (rp.in_end && getenv("BITEDGE_UNAL_RS4")) rs = 4;
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
     const int64_t grid = (threads + kThreads - 1) / kThreads;

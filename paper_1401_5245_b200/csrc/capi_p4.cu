@@ -235,8 +235,8 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }
-    // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items
-    // loaded word by word
+    // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items cut
+    // out of aligned 16-byte chunks (UNAL)
     if (rb % 4 == 0 && al(p4_in, 4) && al(p4_out, 4) && !getenv("BITEDGE_P4_UNFUSED") &&
         !getenv("BITEDGE_P4_BYTES") && n * h < ((int64_t)1 << 31)) {
         RegParams rp;

@@ -51,7 +51,7 @@ struct RegParams {
     uint32_t *o_packed;      // kOutAll only: the packed input, padding 1 (or nullptr)
     int pdl_late;            // K2w: signal dependents after the stores, not at entry
     int oswap;               // K2t2: 1 = uint64 output words (pixel word p at uint32 index p ^ 1)
-    const char *in_end;      // K1 LD4: end of the input buffer (word loads stop there)
+    const char *in_end;      // K1 UNAL: end of the input buffer (loads stop there)
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -157,11 +157,14 @@ inline bool k1_setup(const RegParams &p, K1Div &d) {
 // whole, there are no padding bits and the only border work at the right edge
 // is the fill word to the right of a row's last item, so the per-word tail
 // test (pixel w-1 fill, padding force) is compiled out.
-// LD4: rows are only 4-byte aligned (P4 payloads of w % 32 == 0 or 25..31): the
-// CW words of an item are loaded one by one, and a row's last item may run into
-// the next row (those words are padding positions) but never past `in_end`.
+// UNAL: rows are only 4-byte aligned (packed rows that are not 16-byte multiples,
+// e.g. the drop-in's uint64 words at w = 8000; P4 payloads of w % 32 == 0 or
+// 25..31).  An item's 4 words are cut out of the two aligned 16-byte chunks
+// around them (two vector loads, shared with the neighbouring lanes through L1,
+// and a word select by the row's misalignment); a row's last item may read into
+// the next row (padding positions) but never past `in_end`.  CW must be 4.
 template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false,
-          bool LD4 = false>
+          bool UNAL = false>
 __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
 edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
     pdl_wait();
@@ -195,10 +198,21 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
             if (i == 0 && gi < 0 && p.above) ptr = p.above + 4 * pw0;
             if (i >= 1 && gi == p.nrows && p.below) ptr = p.below + 4 * pw0;   // partial last strip too
         }
-        if constexpr (LD4) {
+        if constexpr (UNAL) {
+            static_assert(CW == 4, "UNAL items are 4 words");
+            const int m = (int)(((uintptr_t)ptr >> 2) & 3);      // word misalignment of the row
+            const char *a0 = ptr - 4 * m;                       // 16-byte aligned
+            if (a0 + 32 <= p.in_end) {
+                const uint4 x = ldg_stream_v4(a0), y = ldg_stream_v4(a0 + 16);
+                const uint32_t t[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
 #pragma unroll
-            for (int q = 0; q < CW; ++q)
-                v[i][q] = ptr + 4 * q + 4 <= p.in_end ? __ldg((const uint32_t *)ptr + q) : 0u;
+                for (int q = 0; q < 4; ++q)
+                    v[i][q] = m == 0 ? t[q] : m == 1 ? t[q + 1] : m == 2 ? t[q + 2] : t[q + 3];
+            } else {                                            // the buffer's last bytes
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    v[i][q] = ptr + 4 * q + 4 <= p.in_end ? __ldg((const uint32_t *)ptr + q) : 0u;
+            }
         } else {
             load_chunk<CW>(ptr, v[i]);               // P4: raw bytes, converted per use
         }

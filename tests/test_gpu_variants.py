@@ -35,10 +35,11 @@ VARIANTS = {
     "k1_generic": {"BITEDGE_K1_GENERIC": "1"},
     "k1_prs2": {"BITEDGE_PRS": "2"},
     "k1_prs8": {"BITEDGE_PRS": "8"},
+    "no_unal": {"BITEDGE_NO_UNAL": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
-SHAPES = [(64, 64, 64), (8, 32, 32), (3, 40, 2048), (2, 70, 4160), (5, 33, 100), (1, 1, 1),
+SHAPES = [(64, 64, 64), (8, 32, 32), (3, 40, 2048), (2, 70, 4160), (5, 33, 100), (1, 1, 1), (3, 50, 8000), (2, 9, 1000),
           (1, 300, 1), (1, 1, 700), (4, 16, 256), (2, 200, 8192)]
 
 
