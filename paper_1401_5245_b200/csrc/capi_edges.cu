@@ -231,6 +231,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     if (unal) {
         if (multi) return kNoKernel;
         rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + (int64_t)G.wp * 4;
+        rp.unal_words = getenv("BITEDGE_UNAL_CHUNKS") == nullptr;   // words: measured faster
     }
     // (uint64 words take 2-row strips only in the tail-free and UNAL kernels)
     const bool swap2 = !G.swap || unal || k1_aligned(o_edges && !o_eset && !multi, cw, G.w);

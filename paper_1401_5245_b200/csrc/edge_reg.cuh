@@ -52,6 +52,7 @@ struct RegParams {
     int pdl_late;            // K2w: signal dependents after the stores, not at entry
     int oswap;               // K2t2: 1 = uint64 output words (pixel word p at uint32 index p ^ 1)
     const char *in_end;      // K1 UNAL: end of the input buffer (loads stop there)
+    int unal_words;          // K1 UNAL: load the 4 words one by one instead of 2 chunks
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -159,10 +160,11 @@ inline bool k1_setup(const RegParams &p, K1Div &d) {
 // test (pixel w-1 fill, padding force) is compiled out.
 // UNAL: rows are only 4-byte aligned (packed rows that are not 16-byte multiples,
 // e.g. the drop-in's uint64 words at w = 8000; P4 payloads of w % 32 == 0 or
-// 25..31).  An item's 4 words are cut out of the two aligned 16-byte chunks
-// around them (two vector loads, shared with the neighbouring lanes through L1,
-// and a word select by the row's misalignment); a row's last item may read into
-// the next row (padding positions) but never past `in_end`.  CW must be 4.
+// 25..31).  An item's 4 words are loaded one by one (default), or cut out of the
+// two aligned 16-byte chunks around them (`unal_words` = 0: two L1-cached vector
+// loads and a word select by the row's misalignment -- measured slower: 8192 x
+// 8000 u32 4.95 vs 4.43 us, 8.6 vs 6.6 us serially); a row's last item may read
+// into the next row (padding positions) but never past `in_end`.  CW must be 4.
 template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false,
           bool UNAL = false>
 __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
@@ -202,8 +204,10 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
             static_assert(CW == 4, "UNAL items are 4 words");
             const int m = (int)(((uintptr_t)ptr >> 2) & 3);      // word misalignment of the row
             const char *a0 = ptr - 4 * m;                       // 16-byte aligned
-            if (a0 + 32 <= p.in_end) {
-                const uint4 x = ldg_stream_v4(a0), y = ldg_stream_v4(a0 + 16);
+            if (!p.unal_words && a0 + 32 <= p.in_end) {
+                // L1-cached: lane L's second chunk is lane L+1's first
+                const uint4 x = __ldg(reinterpret_cast<const uint4 *>(a0));
+                const uint4 y = __ldg(reinterpret_cast<const uint4 *>(a0 + 16));
                 const uint32_t t[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)

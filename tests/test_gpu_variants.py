@@ -36,6 +36,7 @@ VARIANTS = {
     "k1_prs2": {"BITEDGE_PRS": "2"},
     "k1_prs8": {"BITEDGE_PRS": "8"},
     "no_unal": {"BITEDGE_NO_UNAL": "1"},
+    "unal_chunks": {"BITEDGE_UNAL_CHUNKS": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
