@@ -123,6 +123,14 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cu
 
 template <int OUT, bool HALO>
 int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
+    if (rp.in_end != nullptr) {                  // UNAL: rows at any byte, no halos
+        if constexpr (HALO) {
+            return kNoKernel;
+        } else {
+            launch_k(edge_reg_u8_kernel<4, OUT, false, false, true>, grid, 0, st, rp);
+            return cuda_check("edge_reg_u8_kernel<UNAL>");
+        }
+    }
     if (rp.v8) {
         if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, 0, st, rp);
         else launch_k(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, 0, st, rp);
@@ -186,6 +194,32 @@ int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t
     return cuda_check("edge_tma2_u8_kernel");
 }
 
+// K2 UNAL: uint8 rows at any byte offset (see edge_reg_u8_kernel), 4-row strips,
+// edges and / or EdgeSet, uint32 or (oswap) uint64 output words.
+int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uint32_t *o_eset,
+                    int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
+                    int64_t row_hi, cudaStream_t st, int thr) {
+    if (G.h >= ((int64_t)1 << 31)) return kNoKernel;
+    RegParams rp;
+    memset(&rp, 0, sizeof(rp));
+    rp.in = (const char *)in; rp.in_row_bytes = in_row_bytes;
+    rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + G.w;
+    rp.o_edges = o_edges; rp.o_eset = o_eset; rp.out_stride = out_stride_u32;
+    rp.oswap = G.swap;
+    rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
+    rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
+    rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
+    rp.items = G.wp;
+    rp.thr = thr;
+    constexpr int rs = 4;
+    rp.nstrips = (row_hi - row_lo + rs - 1) / rs;
+    const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
+    if (grid > 0x7FFFFFFFLL) return kNoKernel;
+    if (o_edges && o_eset) return launch_reg_u8<kOutAny, false>(rp, rs, (unsigned)grid, st);
+    if (o_eset) return launch_reg_u8<kOutEset, false>(rp, rs, (unsigned)grid, st);
+    return launch_reg_u8<kOutEdges, false>(rp, rs, (unsigned)grid, st);
+}
+
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
             const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
             uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
@@ -198,6 +232,13 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const bool unal = input_kind == 0 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
                       !below && ((uintptr_t)in % 4) == 0 && in_row_bytes % 4 == 0 &&
                       !getenv("BITEDGE_NO_UNAL");
+    // uint8 rows at any byte (row lengths that are not 16-byte multiples): K2's
+    // UNAL strips, single-output, without halos
+    const bool multi0 = o_side[0] || o_side[1] || o_side[2] || o_side[3] || o_packed;
+    const bool u8unal = input_kind == 1 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
+                        !below && !multi0 && !getenv("BITEDGE_NO_UNAL");
+    if (u8unal) return try_reg_u8_unal(in, in_row_bytes, o_edges, o_eset, out_stride_u32, G, nrows,
+                                       row_lo, row_hi, st, thr);
     if (!unal && (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0))
         return kNoKernel;
     if (G.h >= ((int64_t)1 << 31)) return kNoKernel;
@@ -213,7 +254,10 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // swapped halves; it takes every such shape >= 1024 px wide, the tile kernel
     // the rest
     const bool u64_out = input_kind == 1 && G.swap;
-    if (u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"))) return kNoKernel;
+    // uint8 -> uint64 words below 1024 px (or without TMA): K2 stores the swapped
+    // columns (oswap), except for multi-output (tile kernel)
+    const bool u64_k2 = u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"));
+    if (u64_k2 && multi) return kNoKernel;
     rp.oswap = u64_out ? 1 : 0;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
@@ -296,7 +340,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
-    if (input_kind == 1 && (G.w >= 2048 || u64_out) && !getenv("BITEDGE_NO_TMA") &&
+    if (input_kind == 1 && (G.w >= 2048 || (u64_out && !u64_k2)) && !getenv("BITEDGE_NO_TMA") &&
         (!getenv("BITEDGE_TMA1") || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
@@ -314,8 +358,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
-    if ((multi || u64_out) && input_kind == 1) return kNoKernel;   // other uint8 shapes: tile kernel
-    if (input_kind == 1 && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
+    if (multi && input_kind == 1) return kNoKernel;   // other uint8 multi-output: tile kernel
+    if (input_kind == 1 && !u64_out && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
         const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
@@ -346,7 +390,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
     constexpr int kRSL = 32, kQ = 4;
-    if (input_kind == 1 && rp.v8 && !getenv("BITEDGE_NO_ROLL") &&
+    if (input_kind == 1 && rp.v8 && !u64_out && !getenv("BITEDGE_NO_ROLL") &&
         (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
         rp.nstrips = (rows + kRSL - 1) / kRSL;
         const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;

@@ -474,7 +474,12 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
     if (p.pdl_late) pdl_trigger();
 }
 
-template <int RS, int OUT, bool HALO, bool V8>
+// K2 one-shot strips.  UNAL: rows start at any byte (row lengths that are not
+// 16-byte multiples, strided views): a word's 32 bytes come from the 9 aligned
+// 32-bit words around them (L1-cached loads) and one byte permute per word;
+// never read past `in_end`.  Output words go to column c ^ oswap (1: the
+// drop-in's uint64 layout; the u64 row's last u32 word may be pure padding).
+template <int RS, int OUT, bool HALO, bool V8, bool UNAL = false>
 __global__ void __launch_bounds__(kThreads)
 edge_reg_u8_kernel(const RegParams p) {
     pdl_wait();
@@ -491,8 +496,9 @@ edge_reg_u8_kernel(const RegParams p) {
     const int64_t rb = p.in_row_bytes;
     // second 16-byte piece inside the 16-B-rounded row?
     const bool has_hi = x0 + 16 < ((p.w + 15) & ~(int64_t)15);
+    const bool inrow = x0 < p.w;                       // else a pure padding word (u64 rows)
     const bool need_l = live && c > 0 && lane == 0;
-    const bool need_r = live && c + 1 < p.items && lane == 31;
+    const bool need_r = live && c + 1 < p.items && lane == 31 && x0 + 32 < p.w;
 
     const char *base = p.in + (g0 - 1) * rb + x0;
     const int i_lo = g0 == 0 ? 1 : 0;
@@ -511,8 +517,31 @@ edge_reg_u8_kernel(const RegParams p) {
             }
             ra[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
             rb2[i] = ra[i];
-            if (ok) {
-                if (V8) {
+            if (ok && inrow) {
+                if constexpr (UNAL) {
+                    const uintptr_t pa = (uintptr_t)ptr;
+                    const uint32_t *a4 = reinterpret_cast<const uint32_t *>(pa & ~(uintptr_t)3);
+                    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(pa & 3);
+                    uint32_t tw[9];
+                    if ((const char *)(a4 + 9) <= p.in_end) {
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) tw[k] = __ldg(a4 + k);
+                    } else {                                   // the buffer's last bytes
+                        const char *b = reinterpret_cast<const char *>(a4);
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) {
+                            uint32_t v = 0u;
+                            for (int j = 0; j < 4; ++j)
+                                if (b + 4 * k + j < p.in_end)
+                                    v |= (uint32_t)(uint8_t)__ldg(b + 4 * k + j) << (8 * j);
+                            tw[k] = v;
+                        }
+                    }
+                    ra[i] = make_uint4(__byte_perm(tw[0], tw[1], sel), __byte_perm(tw[1], tw[2], sel),
+                                       __byte_perm(tw[2], tw[3], sel), __byte_perm(tw[3], tw[4], sel));
+                    rb2[i] = make_uint4(__byte_perm(tw[4], tw[5], sel), __byte_perm(tw[5], tw[6], sel),
+                                        __byte_perm(tw[6], tw[7], sel), __byte_perm(tw[7], tw[8], sel));
+                } else if (V8) {
                     ldg_stream_v8(ptr, ra[i], rb2[i]);
                 } else {
                     ra[i] = ldg_stream_v4(ptr);
@@ -539,7 +568,7 @@ edge_reg_u8_kernel(const RegParams p) {
         force = 0xFFFFFFFFu;
     }
     uint32_t y = live ? (uint32_t)(g0 % p.h) : 0u;
-    int64_t o = g0 * p.out_stride + c;
+    int64_t o = g0 * p.out_stride + (c ^ p.oswap);
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
         const uint32_t cw = wd[r + 1];
