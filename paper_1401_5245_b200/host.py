@@ -27,7 +27,8 @@ class HostBatchEdges:
 
     def __init__(self, shape, kind: str = "u8", width: int | None = None, border=1,
                  chunk_images: int | None = None, device=None, chunk_rows: int | None = None,
-                 halo_rows: tuple = (False, False), zero_copy: bool | None = None):
+                 halo_rows: tuple = (False, False), zero_copy: bool | None = None,
+                 lanes: int = 2):
         """`halo_rows=(above, below)`: the host input of a single-image row slab
         also holds the row above its first row / below its last row (a row shard
         of a larger raster, multi-GPU); the result covers the slab's own rows.
@@ -63,28 +64,39 @@ class HostBatchEdges:
             chunk_rows is not None or per_img >= (4 << 20) or self.halo_flags != 0)
         if chunk_rows is not None and not self.rows_mode:
             raise ValueError("chunk_rows applies to a single image (n == 1)")
+        # submit() with two lanes moves a batch / image up to 64 / 128 MiB as ONE
+        # chunk: consecutive batches then overlap their copies across the lanes
+        # (C3 e2e 300 -> 321, C2 53.1 -> 53.9 Gpixel/s on one box), while a
+        # blocking __call__ keeps the chunked pipeline inside the call
+        whole_ok = lanes == 2
         if self.rows_mode:
-            if chunk_rows is None:
+            auto = chunk_rows is None
+            if auto:
                 # two equal chunks up to 128 MiB images, then 64 MiB chunks: per-copy
                 # fixed costs make small chunks slow (scripts/c3_e2e.py: C3 0.22 ms
                 # at 2 x 4 MiB vs 0.27 at 4 x 2 MiB; C4 11.2 ms at 64 MiB chunks vs
                 # 12.6 at 8 MiB)
                 chunk_rows = max(1, min(64 << 20, -(-per_img // 2)) // row_bytes)
             self.chunk = int(chunk_rows)                                    # rows per chunk
-            self.d_in = [torch.empty((self.chunk + 2, s), dtype=self.in_dtype, device=self.device)
-                         for _ in range(2)]
-            self.d_out = [torch.empty((self.chunk, self.out_shape[2]), dtype=torch.int32,
-                                      device=self.device) for _ in range(2)]
+            self.submit_chunk = h if (auto and whole_ok and per_img <= (128 << 20)) else self.chunk
+            big = max(self.chunk, self.submit_chunk)
+            self.d_in = [torch.empty((c + 2, s), dtype=self.in_dtype, device=self.device)
+                         for c in (big, self.chunk)]
+            self.d_out = [torch.empty((c, self.out_shape[2]), dtype=torch.int32,
+                                      device=self.device) for c in (big, self.chunk)]
         else:
-            if chunk_images is None:
+            auto = chunk_images is None
+            if auto:
                 # >= 8 MiB chunks, up to 64 MiB for big batches (fewer, larger copies)
                 target = max(8 << 20, min(64 << 20, n * per_img // 8))
                 chunk_images = max(1, min(n, target // max(1, per_img)))
             self.chunk = int(chunk_images)
-            self.d_in = [torch.empty((self.chunk, h, s), dtype=self.in_dtype, device=self.device)
-                         for _ in range(2)]
-            self.d_out = [torch.empty((self.chunk,) + self.out_shape[1:], dtype=torch.int32,
-                                      device=self.device) for _ in range(2)]
+            self.submit_chunk = n if (auto and whole_ok and n * per_img <= (64 << 20)) else self.chunk
+            big = max(self.chunk, self.submit_chunk)
+            self.d_in = [torch.empty((c, h, s), dtype=self.in_dtype, device=self.device)
+                         for c in (big, self.chunk)]
+            self.d_out = [torch.empty((c,) + self.out_shape[1:], dtype=torch.int32,
+                                      device=self.device) for c in (big, self.chunk)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(2)]
         if zero_copy is None:
             zero_copy = (not self.rows_mode and n * per_img <= (4 << 20) and
@@ -93,15 +105,37 @@ class HostBatchEdges:
             raise ValueError("zero_copy needs whole images and, for uint8, rows narrower "
                              "than 1024 px (the wider kernels stage rows with TMA)")
         self.zero_copy = bool(zero_copy)
+        if lanes not in (1, 2):
+            raise ValueError("lanes must be 1 or 2")
+        self.lanes = 1 if self.zero_copy else lanes
         self.h2d_bytes = n * h * s * (1 if kind == "u8" else 4)
-        if self.rows_mode:          # + the halo rows each chunk copies in
-            chunks = -(-h // self.chunk)
+        if self.rows_mode:          # + the halo rows each chunk of a submit() copies in
+            chunks = -(-h // self.submit_chunk)
             extra = 2 * (chunks - 1) + bool(self.halo_flags & 1) + bool(self.halo_flags & 2)
             self.h2d_bytes += extra * row_bytes
         self.d2h_bytes = n * self.out_shape[1] * self.out_shape[2] * 4
         P = ctypes.c_void_p
         self._din = (P * 2)(*[t.data_ptr() for t in self.d_in])
         self._dout = (P * 2)(*[t.data_ptr() for t in self.d_out])
+        # submit() alternates between two lanes (buffers + stream pair): with one
+        # lane, the next batch's first host->device copy waits in stream order for
+        # the previous batch's device->host copies; two lanes let the copy engines
+        # of both directions run back to back (C3 e2e: 79 % -> see DESIGN 5).
+        # Lane 1 is allocated on the first submit.
+        self._lanes = [(self.streams, self._din, self._dout)]
+        self._keep = [self.d_in, self.d_out]
+        self._next = 0
+
+    def _lane(self, k: int):
+        if k >= len(self._lanes):
+            d_in = [torch.empty_like(t) for t in self.d_in]
+            d_out = [torch.empty_like(t) for t in self.d_out]
+            self._keep += [d_in, d_out]
+            P = ctypes.c_void_p
+            self._lanes.append(([torch.cuda.Stream(self.device) for _ in range(2)],
+                                (P * 2)(*[t.data_ptr() for t in d_in]),
+                                (P * 2)(*[t.data_ptr() for t in d_out])))
+        return self._lanes[k]
 
     def new_host_buffers(self):
         hin = torch.empty(self.in_shape, dtype=self.in_dtype, pin_memory=True)
@@ -119,11 +153,13 @@ class HostBatchEdges:
             raise ValueError(f"host output must be a contiguous CPU int32 tensor {self.out_shape}")
         return host_out
 
-    def _run(self, host_in, host_out, blocking: bool) -> None:
+    def _run(self, host_in, host_out, blocking: bool, lane: int = 0, chunk: int | None = None) -> None:
         P = ctypes.c_void_p
+        streams, din, dout = self._lane(lane)
+        chunk = self.chunk if chunk is None else chunk
         if self.zero_copy and host_in.is_pinned() and host_out.is_pinned():
             # one kernel over page-locked host memory (mapped: same address on the device)
-            st = self.streams[0]
+            st = streams[0]
             wp = self.out_shape[2]
             if self.kind == "u8":
                 _capi.call("be_pack_edge_u8", P(host_in.data_ptr()), P(host_out.data_ptr()),
@@ -139,13 +175,13 @@ class HostBatchEdges:
         if self.rows_mode:
             _capi.call("be_host_edges_rows", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                        P(host_out.data_ptr()), self.h, self.width, cu.fill_bit(self.border),
-                       self.halo_flags, self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
-                       P(self.streams[1].cuda_stream), 1 if blocking else 0)
+                       self.halo_flags, din, dout, chunk, P(streams[0].cuda_stream),
+                       P(streams[1].cuda_stream), 1 if blocking else 0)
             return
         _capi.call("be_host_edges", P(host_in.data_ptr()), 1 if self.kind == "u8" else 0,
                    P(host_out.data_ptr()), self.n, self.h, self.width, cu.fill_bit(self.border),
-                   self._din, self._dout, self.chunk, P(self.streams[0].cuda_stream),
-                   P(self.streams[1].cuda_stream), 1 if blocking else 0)
+                   din, dout, chunk, P(streams[0].cuda_stream),
+                   P(streams[1].cuda_stream), 1 if blocking else 0)
 
     def __call__(self, host_in: torch.Tensor, host_out: torch.Tensor | None = None,
                  sync: bool = True) -> torch.Tensor:
@@ -173,9 +209,11 @@ class HostBatchEdges:
         `host_in` must be ready on the host; both buffers must stay untouched
         until `synchronize()` returns."""
         host_out = self._check(host_in, host_out)
-        self._run(host_in, host_out, False)
+        lane = self._next
+        self._next = (self._next + 1) % self.lanes
+        self._run(host_in, host_out, False, lane, self.submit_chunk)
         evs = []
-        for s_ in self.streams:
+        for s_ in self._lane(lane)[0]:
             e = torch.cuda.Event()
             e.record(s_)
             evs.append(e)
