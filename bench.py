@@ -575,27 +575,32 @@ def run_ours(args):
         # ~16 GB of H2D per timed window (C2: ~950 steps, 0.3 s): averages the short
         # PCIe-rate dips seen on these boxes (scripts/e2e_windows.py)
         e2e_steps = max(3, min(steps, int(max(1, 16e9 / max(1, pipe.h2d_bytes)))))
-        houts = [hout, torch.empty_like(hout, pin_memory=True)]
+        # `depth` batches in flight, one per lane of the pipe, each with its own
+        # host output buffer: step i is submitted before step i-depth+1's result
+        # is awaited and read on the host
+        depth = max(2, pipe.lanes)
+        houts = [hout] + [torch.empty_like(hout, pin_memory=True) for _ in range(depth - 1)]
         for _ in range(2):
             pipe(hin, hout)
-        # warm the pipelined (submit) path over both host output buffers for
+        # warm the pipelined (submit) path over every host output buffer for
         # >= 0.25 s: a fresh box's first ~100 ms of PCIe traffic runs slower
-        t_w, k, pw = time.time(), 0, [None, None]
+        t_w, k, pw = time.time(), 0, [None] * depth
         while k < 8 or time.time() - t_w < 0.25:
-            pw[k & 1] = pipe.submit(hin, houts[k & 1])
-            if k > 0:
-                pw[(k - 1) & 1].synchronize()
+            pw[k % depth] = pipe.submit(hin, houts[k % depth])
+            if k >= depth - 1:
+                pw[(k - depth + 1) % depth].synchronize()
             k += 1
-        pw[(k - 1) & 1].synchronize()
+        for j in range(max(0, k - depth + 1), k):
+            pw[j % depth].synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # step i is submitted before step i-1's result is awaited and read on
-        # the host (two host output buffers), so the CPU-side sync latency of
-        # one step and its last chunk's kernel + D2H hide behind the next
-        # step's H2D (HostBatchEdges.submit does not chain batches)
-        pend = [None, None]
+        # step i is submitted before step i-depth+1's result is awaited and read
+        # on the host (`depth` host output buffers), so the CPU-side sync latency
+        # and each step's kernel + D2H hide behind the following steps' H2D
+        # (HostBatchEdges.submit does not chain batches; a lane per step in flight)
+        pend = [None] * depth
         # timed in windows; the reported rate is the median window's (robust to
         # the transient PCIe-rate dips of these boxes, scripts/e2e_windows.py)
         nwin = 5 if e2e_steps >= 10 else 1
@@ -606,12 +611,13 @@ def run_ours(args):
             e0.record()
             e0.synchronize()                 # every submitted copy starts after e0
             for i in range(per_win):
-                pend[i & 1] = pipe.submit(hin, houts[i & 1])
-                if i > 0:
-                    res = pend[(i - 1) & 1].synchronize()
-                    _ = int(res[0, 0, 0])    # step i-1's result, on the host
-            res = pend[(per_win - 1) & 1].synchronize()
-            _ = int(res[0, 0, 0])
+                pend[i % depth] = pipe.submit(hin, houts[i % depth])
+                if i >= depth - 1:
+                    res = pend[(i - depth + 1) % depth].synchronize()
+                    _ = int(res[0, 0, 0])    # step i-depth+1's result, on the host
+            for j in range(max(0, per_win - depth + 1), per_win):
+                res = pend[j % depth].synchronize()
+                _ = int(res[0, 0, 0])
             e1.record()
             torch.cuda.synchronize()
             wms.append(e0.elapsed_time(e1))

@@ -28,7 +28,7 @@ class HostBatchEdges:
     def __init__(self, shape, kind: str = "u8", width: int | None = None, border=1,
                  chunk_images: int | None = None, device=None, chunk_rows: int | None = None,
                  halo_rows: tuple = (False, False), zero_copy: bool | None = None,
-                 lanes: int = 2):
+                 lanes: int = 3):
         """`halo_rows=(above, below)`: the host input of a single-image row slab
         also holds the row above its first row / below its last row (a row shard
         of a larger raster, multi-GPU); the result covers the slab's own rows.
@@ -64,11 +64,11 @@ class HostBatchEdges:
             chunk_rows is not None or per_img >= (4 << 20) or self.halo_flags != 0)
         if chunk_rows is not None and not self.rows_mode:
             raise ValueError("chunk_rows applies to a single image (n == 1)")
-        # submit() with two lanes moves a batch / image up to 64 / 128 MiB as ONE
-        # chunk: consecutive batches then overlap their copies across the lanes
+        # submit() with several lanes moves a batch / image up to 64 / 128 MiB as
+        # ONE chunk: consecutive batches then overlap their copies across the lanes
         # (C3 e2e 300 -> 321, C2 53.1 -> 53.9 Gpixel/s on one box), while a
         # blocking __call__ keeps the chunked pipeline inside the call
-        whole_ok = lanes == 2
+        whole_ok = lanes >= 2
         if self.rows_mode:
             auto = chunk_rows is None
             if auto:
@@ -105,8 +105,8 @@ class HostBatchEdges:
             raise ValueError("zero_copy needs whole images and, for uint8, rows narrower "
                              "than 1024 px (the wider kernels stage rows with TMA)")
         self.zero_copy = bool(zero_copy)
-        if lanes not in (1, 2):
-            raise ValueError("lanes must be 1 or 2")
+        if lanes not in (1, 2, 3, 4):
+            raise ValueError("lanes must be 1..4")
         self.lanes = 1 if self.zero_copy else lanes
         self.h2d_bytes = n * h * s * (1 if kind == "u8" else 4)
         if self.rows_mode:          # + the halo rows each chunk of a submit() copies in
@@ -117,11 +117,11 @@ class HostBatchEdges:
         P = ctypes.c_void_p
         self._din = (P * 2)(*[t.data_ptr() for t in self.d_in])
         self._dout = (P * 2)(*[t.data_ptr() for t in self.d_out])
-        # submit() alternates between two lanes (buffers + stream pair): with one
+        # submit() cycles through `lanes` lanes (buffers + stream pair): with one
         # lane, the next batch's first host->device copy waits in stream order for
-        # the previous batch's device->host copies; two lanes let the copy engines
-        # of both directions run back to back (C3 e2e: 79 % -> see DESIGN 5).
-        # Lane 1 is allocated on the first submit.
+        # the previous batch's device->host copies; with a lane per batch in
+        # flight the copy engines of both directions run back to back (DESIGN 5).
+        # Lanes past the first are allocated on first use.
         self._lanes = [(self.streams, self._din, self._dout)]
         self._keep = [self.d_in, self.d_out]
         self._next = 0
