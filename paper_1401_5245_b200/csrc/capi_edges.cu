@@ -127,7 +127,10 @@ int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
         if constexpr (HALO) {
             return kNoKernel;
         } else {
-            launch_k(edge_reg_u8_kernel<4, OUT, false, false, true>, grid, 0, st, rp);
+            // widest alignment every row start has (rp.v8 carries it: 8, 4 or 1)
+            if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, 0, st, rp);
+            else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, 0, st, rp);
+            else launch_k(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, 0, st, rp);
             return cuda_check("edge_reg_u8_kernel<UNAL>");
         }
     }
@@ -211,6 +214,11 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
     rp.items = G.wp;
     rp.thr = thr;
+    {   // alignment of every row start (base and row stride)
+        const uintptr_t a = (uintptr_t)in | (uintptr_t)in_row_bytes;
+        rp.v8 = (a % 8 == 0 && !getenv("BITEDGE_UNAL_BYTES")) ? 8
+              : (a % 4 == 0 && !getenv("BITEDGE_UNAL_BYTES")) ? 4 : 1;
+    }
     constexpr int rs = 4;
     rp.nstrips = (row_hi - row_lo + rs - 1) / rs;
     const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;

@@ -479,7 +479,7 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
 // 32-bit words around them (L1-cached loads) and one byte permute per word;
 // never read past `in_end`.  Output words go to column c ^ oswap (1: the
 // drop-in's uint64 layout; the u64 row's last u32 word may be pure padding).
-template <int RS, int OUT, bool HALO, bool V8, bool UNAL = false>
+template <int RS, int OUT, bool HALO, bool V8, int UNAL = 0>   // UNAL: 0, 1 (any byte), 4, 8 (row alignment)
 __global__ void __launch_bounds__(kThreads)
 edge_reg_u8_kernel(const RegParams p) {
     pdl_wait();
@@ -518,7 +518,35 @@ edge_reg_u8_kernel(const RegParams p) {
             ra[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
             rb2[i] = ra[i];
             if (ok && inrow) {
-                if constexpr (UNAL) {
+                if constexpr (UNAL == 8 || UNAL == 4) {
+                    // rows 8- / 4-byte aligned: the 32 bytes as 4 x 64-bit / 8 x 32-bit
+                    // loads (a row's last word may read into the next row, never past
+                    // in_end)
+                    uint32_t tw[8];
+                    if (ptr + 32 <= p.in_end) {
+                        if constexpr (UNAL == 8) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint2 q = __ldg(reinterpret_cast<const uint2 *>(ptr) + k);
+                                tw[2 * k] = q.x; tw[2 * k + 1] = q.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) tw[k] = __ldg(reinterpret_cast<const uint32_t *>(ptr) + k);
+                        }
+                    } else {                                   // the buffer's last bytes
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            uint32_t v = 0u;
+                            for (int j = 0; j < 4; ++j)
+                                if (ptr + 4 * k + j < p.in_end)
+                                    v |= (uint32_t)(uint8_t)__ldg(ptr + 4 * k + j) << (8 * j);
+                            tw[k] = v;
+                        }
+                    }
+                    ra[i] = make_uint4(tw[0], tw[1], tw[2], tw[3]);
+                    rb2[i] = make_uint4(tw[4], tw[5], tw[6], tw[7]);
+                } else if constexpr (UNAL == 1) {
                     const uintptr_t pa = (uintptr_t)ptr;
                     const uint32_t *a4 = reinterpret_cast<const uint32_t *>(pa & ~(uintptr_t)3);
                     const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(pa & 3);

@@ -37,6 +37,7 @@ VARIANTS = {
     "k1_prs8": {"BITEDGE_PRS": "8"},
     "no_unal": {"BITEDGE_NO_UNAL": "1"},
     "unal_chunks": {"BITEDGE_UNAL_CHUNKS": "1"},
+    "unal_bytes": {"BITEDGE_UNAL_BYTES": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
