@@ -524,15 +524,20 @@ edge_reg_u8_kernel(const RegParams p) {
                     // in_end)
                     uint32_t tw[8];
                     if (ptr + 32 <= p.in_end) {
-                        if constexpr (UNAL == 8) {
+                        if (UNAL == 8 || ((uintptr_t)ptr & 7) == 0) {   // this row 8-byte aligned
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const uint2 q = __ldg(reinterpret_cast<const uint2 *>(ptr) + k);
                                 tw[2 * k] = q.x; tw[2 * k + 1] = q.y;
                             }
-                        } else {
+                        } else {                        // 4 mod 8: 32 + 3 x 64 + 32 bits
+                            tw[0] = __ldg(reinterpret_cast<const uint32_t *>(ptr));
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) tw[k] = __ldg(reinterpret_cast<const uint32_t *>(ptr) + k);
+                            for (int k = 0; k < 3; ++k) {
+                                const uint2 q = __ldg(reinterpret_cast<const uint2 *>(ptr + 4) + k);
+                                tw[2 * k + 1] = q.x; tw[2 * k + 2] = q.y;
+                            }
+                            tw[7] = __ldg(reinterpret_cast<const uint32_t *>(ptr) + 7);
                         }
                     } else {                                   // the buffer's last bytes
 #pragma unroll
