@@ -151,7 +151,10 @@ inline bool multi_out(const RegParams &rp) {
 template <bool HALO>
 int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
                     cudaStream_t st) {
-    if (multi_out(rp)) {          // packed input only (uint8 multi-output goes to K2t2 or tile)
+    const bool sides = rp.o_side[0] || rp.o_side[1] || rp.o_side[2] || rp.o_side[3];
+    if (input_kind == 1 && rp.o_packed && !sides && (rp.o_edges || rp.o_eset)) {
+        // uint8: edges and / or EdgeSet plus the packed words -- K2 stores all
+    } else if (multi_out(rp)) {   // packed input only (other uint8 multi-output: K2t2 or tile)
         if (input_kind == 1) return kNoKernel;
         return launch_reg_packed<kOutAll, HALO>(rp, swap, cw, rs, grid, st);
     }
@@ -200,7 +203,7 @@ int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t
 // K2 UNAL: uint8 rows at any byte offset (see edge_reg_u8_kernel), 4-row strips,
 // edges and / or EdgeSet, uint32 or (oswap) uint64 output words.
 int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uint32_t *o_eset,
-                    int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
+                    uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows, int64_t row_lo,
                     int64_t row_hi, cudaStream_t st, int thr) {
     if (G.h >= ((int64_t)1 << 31)) return kNoKernel;
     RegParams rp;
@@ -208,6 +211,7 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     rp.in = (const char *)in; rp.in_row_bytes = in_row_bytes;
     rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + G.w;
     rp.o_edges = o_edges; rp.o_eset = o_eset; rp.out_stride = out_stride_u32;
+    rp.o_packed = o_packed;
     rp.oswap = G.swap;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
@@ -242,10 +246,10 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                       !getenv("BITEDGE_NO_UNAL");
     // uint8 rows at any byte (row lengths that are not 16-byte multiples): K2's
     // UNAL strips, single-output, without halos
-    const bool multi0 = o_side[0] || o_side[1] || o_side[2] || o_side[3] || o_packed;
+    const bool sides0 = o_side[0] || o_side[1] || o_side[2] || o_side[3];
     const bool u8unal = input_kind == 1 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
-                        !below && !multi0 && !getenv("BITEDGE_NO_UNAL");
-    if (u8unal) return try_reg_u8_unal(in, in_row_bytes, o_edges, o_eset, out_stride_u32, G, nrows,
+                        !below && !sides0 && (o_edges || o_eset) && !getenv("BITEDGE_NO_UNAL");
+    if (u8unal) return try_reg_u8_unal(in, in_row_bytes, o_edges, o_eset, o_packed, out_stride_u32, G, nrows,
                                        row_lo, row_hi, st, thr);
     if (!unal && (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0))
         return kNoKernel;
@@ -265,7 +269,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // uint8 -> uint64 words below 1024 px (or without TMA): K2 stores the swapped
     // columns (oswap), except for multi-output (tile kernel)
     const bool u64_k2 = u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"));
-    if (u64_k2 && multi) return kNoKernel;
+    // K2 writes edges / EdgeSet plus, optionally, the packed words; nothing else
+    const bool k2_outs = !sides0 && (o_edges || o_eset);
+    if (u64_k2 && !k2_outs) return kNoKernel;
     rp.oswap = u64_out ? 1 : 0;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
     rp.h = (uint32_t)G.h; rp.w = G.w; rp.wp = G.wp; rp.pl = G.pl;
@@ -366,8 +372,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
-    if (multi && input_kind == 1) return kNoKernel;   // other uint8 multi-output: tile kernel
-    if (input_kind == 1 && !u64_out && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
+    if (!k2_outs && input_kind == 1) return kNoKernel;   // other uint8 multi-output: tile kernel
+    if (input_kind == 1 && !u64_out && !o_packed && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
         const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
@@ -398,7 +404,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
     constexpr int kRSL = 32, kQ = 4;
-    if (input_kind == 1 && rp.v8 && !u64_out && !getenv("BITEDGE_NO_ROLL") &&
+    if (input_kind == 1 && rp.v8 && !u64_out && !o_packed && !getenv("BITEDGE_NO_ROLL") &&
         (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
         rp.nstrips = (rows + kRSL - 1) / kRSL;
         const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;

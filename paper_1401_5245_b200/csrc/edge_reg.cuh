@@ -619,6 +619,7 @@ edge_reg_u8_kernel(const RegParams p) {
             const uint32_t any = ln | rn | u | d;
             if (OUT != kOutEset) __stcs(p.o_edges + o, cw | ~any | force);
             if (OUT != kOutEdges) __stcs(p.o_eset + o, (~cw & any) | force);
+            if (p.o_packed) __stcs(p.o_packed + o, cw | force);   // from_array's words
         }
         o += p.out_stride;
         if (++y == p.h) y = 0;
