@@ -152,8 +152,8 @@ template <bool HALO>
 int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, unsigned grid,
                     cudaStream_t st) {
     const bool sides = rp.o_side[0] || rp.o_side[1] || rp.o_side[2] || rp.o_side[3];
-    if (input_kind == 1 && rp.o_packed && !sides && (rp.o_edges || rp.o_eset)) {
-        // uint8: edges and / or EdgeSet plus the packed words -- K2 stores all
+    if (input_kind == 1 && rp.o_packed && !sides) {
+        // uint8: the packed words, with or without edges / EdgeSet -- K2 stores all
     } else if (multi_out(rp)) {   // packed input only (other uint8 multi-output: K2t2 or tile)
         if (input_kind == 1) return kNoKernel;
         return launch_reg_packed<kOutAll, HALO>(rp, swap, cw, rs, grid, st);
@@ -248,7 +248,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // UNAL strips, single-output, without halos
     const bool sides0 = o_side[0] || o_side[1] || o_side[2] || o_side[3];
     const bool u8unal = input_kind == 1 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
-                        !below && !sides0 && (o_edges || o_eset) && !getenv("BITEDGE_NO_UNAL");
+                        !below && !sides0 && (o_edges || o_eset || o_packed) &&
+                        !getenv("BITEDGE_NO_UNAL");
     if (u8unal) return try_reg_u8_unal(in, in_row_bytes, o_edges, o_eset, o_packed, out_stride_u32, G, nrows,
                                        row_lo, row_hi, st, thr);
     if (!unal && (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0))
@@ -270,7 +271,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // columns (oswap), except for multi-output (tile kernel)
     const bool u64_k2 = u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"));
     // K2 writes edges / EdgeSet plus, optionally, the packed words; nothing else
-    const bool k2_outs = !sides0 && (o_edges || o_eset);
+    const bool k2_outs = !sides0 && (o_edges || o_eset || o_packed);
     if (u64_k2 && !k2_outs) return kNoKernel;
     rp.oswap = u64_out ? 1 : 0;
     rp.nrows = nrows; rp.row_lo = row_lo; rp.row_hi = row_hi;
@@ -358,7 +359,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         (!getenv("BITEDGE_TMA1") || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
-        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr || u64_out;
+        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr || (u64_out && getenv("BITEDGE_U64_TMA"));
         if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
             // strips, so the last wave's tail is a quarter as long: C5 737 ->

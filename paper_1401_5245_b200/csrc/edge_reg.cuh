@@ -617,7 +617,7 @@ edge_reg_u8_kernel(const RegParams p) {
             const uint32_t ln = __funnelshift_r(cw, lw, 1);
             const uint32_t rn = (__funnelshift_l(rw, cw, 1) & keep) | fixb;
             const uint32_t any = ln | rn | u | d;
-            if (OUT != kOutEset) __stcs(p.o_edges + o, cw | ~any | force);
+            if (OUT != kOutEset && p.o_edges) __stcs(p.o_edges + o, cw | ~any | force);
             if (OUT != kOutEdges) __stcs(p.o_eset + o, (~cw & any) | force);
             if (p.o_packed) __stcs(p.o_packed + o, cw | force);   // from_array's words
         }

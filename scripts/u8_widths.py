@@ -39,14 +39,16 @@ for (n, h, w) in ((1, 4096, 4096), (1, 4096, 4100), (1, 4096, 4000), (16, 1024, 
     nbytes = n * h * w
     pool = max(2, min(48, (3 * 126 << 20) // nbytes + 1))
     ins = [torch.randint(0, 2, (n, h, w), dtype=torch.uint8, device=dev) for _ in range(pool)]
-    for wb in (32, 64):
+    for wb in (32, 64, "pack"):
         def step(i):
             if wb == 32:
                 cu.pack_edges_u8(ins[i % pool], 1)
-            else:
+            elif wb == 64:
                 cu.pack_and_edges(ins[i % pool], 1, word_bits=64)
+            else:
+                cu.pack_u8(ins[i % pool], word_bits=64)
         k = pool * max(1, 96 // pool)
         us3, us1 = timed(step, k, 3), timed(step, k, 1)
-        alg = nbytes * 1.125 if wb == 32 else nbytes * 1.25
+        alg = nbytes * 1.125 if wb != 64 else nbytes * 1.25
         print(f"u8->{wb} {n}x{h}x{w}: {us3:7.2f} us ({alg / us3 / 1e3 / 6540.5:.3f}), serial {us1:7.2f} us "
               f"({alg / us1 / 1e3 / 6540.5:.3f})", flush=True)

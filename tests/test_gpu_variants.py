@@ -38,6 +38,7 @@ VARIANTS = {
     "no_unal": {"BITEDGE_NO_UNAL": "1"},
     "unal_chunks": {"BITEDGE_UNAL_CHUNKS": "1"},
     "unal_bytes": {"BITEDGE_UNAL_BYTES": "1"},
+    "u64_tma": {"BITEDGE_U64_TMA": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
