@@ -211,9 +211,11 @@ class HostBatchEdges:
         host_out = self._check(host_in, host_out)
         lane = self._next
         self._next = (self._next + 1) % self.lanes
+        zc = self.zero_copy and host_in.is_pinned() and host_out.is_pinned()
         self._run(host_in, host_out, False, lane, self.submit_chunk)
         evs = []
-        for s_ in self._lane(lane)[0]:
+        # the zero-copy kernel runs on the lane's first stream only
+        for s_ in self._lane(lane)[0][:1 if zc else 2]:
             e = torch.cuda.Event()
             e.record(s_)
             evs.append(e)
