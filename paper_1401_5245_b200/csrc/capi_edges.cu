@@ -263,12 +263,10 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     for (int k = 0; k < 4; ++k) rp.o_side[k] = o_side[k];
     rp.o_packed = o_packed;
     const bool multi = multi_out(rp);
-    // uint8 -> uint64 words (the drop-in BitImage layout): only K2t2 stores
-    // swapped halves; it takes every such shape >= 1024 px wide, the tile kernel
-    // the rest
+    // uint8 -> uint64 words (the drop-in BitImage layout): K2t2 (large rasters
+    // >= 1024 px wide) and K2 store the swapped halves (oswap); K2w / K2r / K2t do
+    // not, and the four side outputs go to the tile kernel
     const bool u64_out = input_kind == 1 && G.swap;
-    // uint8 -> uint64 words below 1024 px (or without TMA): K2 stores the swapped
-    // columns (oswap), except for multi-output (tile kernel)
     const bool u64_k2 = u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"));
     // K2 writes edges / EdgeSet plus, optionally, the packed words; nothing else
     const bool k2_outs = !sides0 && (o_edges || o_eset || o_packed);
@@ -279,7 +277,6 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
     auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
     const bool in32 = al(in, 32) && in_row_bytes % 32 == 0 && al(above, 32) && al(below, 32);
-    // packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4
     // Packed items are 8 words (256-bit loads) when rows are 32-byte aligned, else 4.
     // Small rasters (< 4 waves of 4-row strips) use 2-row strips instead, which
     // doubles the threads in flight (C3: 5.1 us serial / 88 % overlapped vs
