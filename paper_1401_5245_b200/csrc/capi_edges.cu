@@ -64,10 +64,11 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 
 // ---------------------------------------------------------------- register-direct kernel
 
-// K1's tail-free (ALIGNED) instantiations apply: edges only, 8-word items, whole
-// items with no padding bits (BITEDGE_K1_GENERIC turns them off).
-inline bool k1_aligned(bool edges_only, int cw, int64_t w) {
-    return edges_only && cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
+// K1's tail-free (ALIGNED) instantiations apply: edges and / or EdgeSet (not the
+// kOutAll multi-output), 8-word items, whole items with no padding bits
+// (BITEDGE_K1_GENERIC turns them off).
+inline bool k1_aligned(bool single, int cw, int64_t w) {
+    return single && cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
 }
 
 // Launch helpers: dispatch the runtime choices onto template parameters.
@@ -94,7 +95,7 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cu
     } else {
         // whole 8-word items with no padding (w % 256 == 0: C3, C4, and the drop-in's
         // uint64 BitImage words at those widths): the tail-free kernels
-        const bool aligned = k1_aligned(OUT == kOutEdges, cw, rp.w);
+        const bool aligned = k1_aligned(OUT != kOutAll, cw, rp.w);
         if (aligned && swap && rs == 2) {
             launch_k(edge_reg_packed_kernel<1, 2, 8, OUT, HALO, false, true>, grid, 0, st, rp, dv);
         } else if (aligned && swap && rs == 4) {
@@ -290,7 +291,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         rp.unal_words = getenv("BITEDGE_UNAL_CHUNKS") == nullptr;   // words: measured faster
     }
     // (uint64 words take 2-row strips only in the tail-free and UNAL kernels)
-    const bool swap2 = !G.swap || unal || k1_aligned(o_edges && !o_eset && !multi, cw, G.w);
+    const bool swap2 = !G.swap || unal || k1_aligned(!multi, cw, G.w);
     const int packed_rs = (input_kind == 0 && swap2 && !big) ? 2 : 4;
     if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
