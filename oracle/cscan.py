@@ -33,8 +33,14 @@ def lib():
         L.orc_scan_p32_slab.argtypes = [_P, _P, _P, _P, _I64, _I64, _I64, _INT]
         for f in (L.orc_scan_u8_packed32, L.orc_scan_p32, L.orc_scan_p32_slab):
             f.restype = None
+        L.orc_threads.restype = _INT
         _lib = L
     return _lib
+
+
+def threads() -> int:
+    """Worker threads each scan uses (ORACLE_THREADS, default all online cores)."""
+    return int(lib().orc_threads())
 
 
 def _ptr(a: np.ndarray):

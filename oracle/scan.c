@@ -9,9 +9,10 @@
  * words with padding bits = 1 (bitimage.py:1-11, 101-104).
  *
  * This is an algorithm independent of the word-level mask method, fast enough
- * (pthreads over rows) to check the full-size BASELINE configs (C4: 4 Gpx, C5:
- * 4 Gpx) where the numpy port (oracle/port.py) is too slow.  Only tests/ and
- * bench.py's CPU legs may load it.
+ * to check the full-size BASELINE configs (C4: 4 Gpx, C5: 4 Gpx) where the
+ * numpy port (oracle/port.py) is too slow: every scanner splits its rows over
+ * ORACLE_THREADS (default: all online cores) pthreads with parallel_for.
+ * Only tests/ and bench.py's CPU legs may load it.
  */
 #include <pthread.h>
 #include <stdint.h>
@@ -19,7 +20,7 @@
 #include <string.h>
 #include <unistd.h>
 
-/* Minimal pthread parallel-for over [0, total) (no OpenMP runtime in the image). */
+/* Minimal pthread parallel-for over [0, total) (no OpenMP runtime dependency). */
 typedef void (*range_fn)(void *ctx, int64_t lo, int64_t hi);
 typedef struct { range_fn fn; void *ctx; int64_t lo, hi; } job_t;
 
@@ -76,14 +77,19 @@ static inline int px_p32(const uint32_t *img, int64_t h, int64_t w, int64_t stri
 
 /* in: uint8 [n, h, w] with row stride `in_stride` bytes (image stride h*in_stride);
  * out: uint32 [n, h, ceil(w/32)] contiguous. */
-void orc_scan_u8_packed32(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
-                          int64_t in_stride, int fill, int edgeset) {
+typedef struct {
+    const uint8_t *in; uint32_t *out; int64_t h, w, in_stride; int fill, edgeset;
+} scan_u8_ctx;
+
+static void scan_u8_rows(void *vctx, int64_t lo, int64_t hi) {
+    const scan_u8_ctx *c = (const scan_u8_ctx *)vctx;
+    const int64_t h = c->h, w = c->w, in_stride = c->in_stride;
+    const int fill = c->fill, edgeset = c->edgeset;
     const int64_t wp = (w + 31) / 32;
-#pragma omp parallel for schedule(static)
-    for (int64_t ry = 0; ry < n * h; ++ry) {
+    for (int64_t ry = lo; ry < hi; ++ry) {
         const int64_t img_i = ry / h, y = ry % h;
-        const uint8_t *img = in + img_i * h * in_stride;
-        uint32_t *orow = out + ry * wp;
+        const uint8_t *img = c->in + img_i * h * in_stride;
+        uint32_t *orow = c->out + ry * wp;
         for (int64_t k = 0; k < wp; ++k) {
             uint32_t word = 0;
             for (int b = 0; b < 32; ++b) {
@@ -101,16 +107,27 @@ void orc_scan_u8_packed32(const uint8_t *in, uint32_t *out, int64_t n, int64_t h
     }
 }
 
+void orc_scan_u8_packed32(const uint8_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                          int64_t in_stride, int fill, int edgeset) {
+    scan_u8_ctx c = {in, out, h, w, in_stride, fill, edgeset};
+    parallel_for(n * h, scan_u8_rows, &c);
+}
+
 /* in: packed uint32 rows [n, h, in_stride words] (padding bits ignored);
  * out: uint32 [n, h, ceil(w/32)] contiguous. */
-void orc_scan_p32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
-                  int64_t in_stride, int fill, int edgeset) {
+typedef struct {
+    const uint32_t *in; uint32_t *out; int64_t h, w, in_stride; int fill, edgeset;
+} scan_p32_ctx;
+
+static void scan_p32_rows(void *vctx, int64_t lo, int64_t hi) {
+    const scan_p32_ctx *c = (const scan_p32_ctx *)vctx;
+    const int64_t h = c->h, w = c->w, in_stride = c->in_stride;
+    const int fill = c->fill, edgeset = c->edgeset;
     const int64_t wp = (w + 31) / 32;
-#pragma omp parallel for schedule(static)
-    for (int64_t ry = 0; ry < n * h; ++ry) {
+    for (int64_t ry = lo; ry < hi; ++ry) {
         const int64_t img_i = ry / h, y = ry % h;
-        const uint32_t *img = in + img_i * h * in_stride;
-        uint32_t *orow = out + ry * wp;
+        const uint32_t *img = c->in + img_i * h * in_stride;
+        uint32_t *orow = c->out + ry * wp;
         for (int64_t k = 0; k < wp; ++k) {
             uint32_t word = 0;
             for (int b = 0; b < 32; ++b) {
@@ -128,14 +145,25 @@ void orc_scan_p32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64
     }
 }
 
+void orc_scan_p32(const uint32_t *in, uint32_t *out, int64_t n, int64_t h, int64_t w,
+                  int64_t in_stride, int fill, int edgeset) {
+    scan_p32_ctx c = {in, out, h, w, in_stride, fill, edgeset};
+    parallel_for(n * h, scan_p32_rows, &c);
+}
+
 /* Row-slab variant: rows [0, rows) of a slab whose global neighbours above
  * (row -1) and below (row `rows`) come from `above` / `below` (NULL -> fill).
  * Used to check the row-sharded (halo) path. */
-void orc_scan_p32_slab(const uint32_t *slab, const uint32_t *above, const uint32_t *below,
-                       uint32_t *out, int64_t rows, int64_t w, int64_t stride, int fill) {
+typedef struct {
+    const uint32_t *slab, *above, *below; uint32_t *out; int64_t rows, w, stride; int fill;
+} scan_slab_ctx;
+
+static void scan_slab_rows(void *vctx, int64_t lo, int64_t hi) {
+    const scan_slab_ctx *c = (const scan_slab_ctx *)vctx;
+    const int64_t rows = c->rows, w = c->w, stride = c->stride;
+    const int fill = c->fill;
     const int64_t wp = (w + 31) / 32;
-#pragma omp parallel for schedule(static)
-    for (int64_t y = 0; y < rows; ++y) {
+    for (int64_t y = lo; y < hi; ++y) {
         for (int64_t k = 0; k < wp; ++k) {
             uint32_t word = 0;
             for (int b = 0; b < 32; ++b) {
@@ -143,21 +171,27 @@ void orc_scan_p32_slab(const uint32_t *slab, const uint32_t *above, const uint32
                 int bit = 1;
                 if (x < w) {
                     int nb[4];
-                    int c = px_p32(slab, rows, w, stride, x, y, fill);
-                    nb[0] = px_p32(slab, rows, w, stride, x - 1, y, fill);
-                    nb[1] = px_p32(slab, rows, w, stride, x + 1, y, fill);
-                    if (y > 0) nb[2] = px_p32(slab, rows, w, stride, x, y - 1, fill);
-                    else nb[2] = above ? px_p32(above, 1, w, stride, x, 0, fill) : fill;
-                    if (y + 1 < rows) nb[3] = px_p32(slab, rows, w, stride, x, y + 1, fill);
-                    else nb[3] = below ? px_p32(below, 1, w, stride, x, 0, fill) : fill;
-                    int e = !c && (nb[0] | nb[1] | nb[2] | nb[3]);
+                    int cc = px_p32(c->slab, rows, w, stride, x, y, fill);
+                    nb[0] = px_p32(c->slab, rows, w, stride, x - 1, y, fill);
+                    nb[1] = px_p32(c->slab, rows, w, stride, x + 1, y, fill);
+                    if (y > 0) nb[2] = px_p32(c->slab, rows, w, stride, x, y - 1, fill);
+                    else nb[2] = c->above ? px_p32(c->above, 1, w, stride, x, 0, fill) : fill;
+                    if (y + 1 < rows) nb[3] = px_p32(c->slab, rows, w, stride, x, y + 1, fill);
+                    else nb[3] = c->below ? px_p32(c->below, 1, w, stride, x, 0, fill) : fill;
+                    int e = !cc && (nb[0] | nb[1] | nb[2] | nb[3]);
                     bit = !e;
                 }
                 word = (word << 1) | (uint32_t)bit;
             }
-            out[y * wp + k] = word;
+            c->out[y * wp + k] = word;
         }
     }
+}
+
+void orc_scan_p32_slab(const uint32_t *slab, const uint32_t *above, const uint32_t *below,
+                       uint32_t *out, int64_t rows, int64_t w, int64_t stride, int fill) {
+    scan_slab_ctx c = {slab, above, below, out, rows, w, stride, fill};
+    parallel_for(rows, scan_slab_rows, &c);
 }
 
 int orc_version(void) { return 1; }

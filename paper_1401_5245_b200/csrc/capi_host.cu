@@ -61,6 +61,46 @@ int be_ipc_close(void *dev_ptr, int64_t offset) {
     return BE_OK;
 }
 
+// ---- device-side producer -> consumer handshake for peer halos -------------
+// Stream memory operations (cuStreamWaitValue32 / cuStreamWriteValue32, looked up
+// through the runtime's driver entry point so the library does not link libcuda):
+// the GPU front end waits for / writes a 32-bit word in device or IPC peer memory
+// in stream order -- no kernel spins, no host round trip.
+typedef int (*cuStreamWaitValue32_t)(void *, unsigned long long, uint32_t, unsigned int);
+typedef int (*cuStreamWriteValue32_t)(void *, unsigned long long, uint32_t, unsigned int);
+
+static void *driver_fn(const char *name) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return fn;
+}
+
+int be_stream_wait_geq32(const void *flag, uint32_t value, void *stream) {
+    if (flag == nullptr) return fail(BE_EINVAL, "NULL flag");
+    if (((uintptr_t)flag & 3) != 0) return fail(BE_EINVAL, "flag must be 4-byte aligned");
+    static cuStreamWaitValue32_t fn = (cuStreamWaitValue32_t)driver_fn("cuStreamWaitValue32");
+    if (fn == nullptr) return fail(BE_EINVAL, "cuStreamWaitValue32 unavailable");
+    // CU_STREAM_WAIT_VALUE_GEQ = 0: (int32_t)(*flag - value) >= 0
+    int r = fn(stream, (unsigned long long)(uintptr_t)flag, value, 0x0);
+    if (r != 0) return fail(r, "cuStreamWaitValue32 failed (CUresult %d)", r);
+    return BE_OK;
+}
+
+int be_stream_write32(void *flag, uint32_t value, void *stream) {
+    if (flag == nullptr) return fail(BE_EINVAL, "NULL flag");
+    if (((uintptr_t)flag & 3) != 0) return fail(BE_EINVAL, "flag must be 4-byte aligned");
+    static cuStreamWriteValue32_t fn = (cuStreamWriteValue32_t)driver_fn("cuStreamWriteValue32");
+    if (fn == nullptr) return fail(BE_EINVAL, "cuStreamWriteValue32 unavailable");
+    // CU_STREAM_WRITE_VALUE_DEFAULT = 0: ordered after (and with a memory barrier
+    // behind) all prior work on the stream
+    int r = fn(stream, (unsigned long long)(uintptr_t)flag, value, 0x0);
+    if (r != 0) return fail(r, "cuStreamWriteValue32 failed (CUresult %d)", r);
+    return BE_OK;
+}
+
 int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
                   int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
                   int64_t chunk_images, void *stream0, void *stream1, int blocking) {

@@ -99,8 +99,15 @@ def _packed(words: torch.Tensor, width: int, what: str = "words"):
     return w3, wb, rs
 
 
-def _new_like(w3: torch.Tensor, squeeze: bool) -> torch.Tensor:
-    out = torch.empty(w3.shape, dtype=w3.dtype, device=w3.device)
+def _new_like(w3: torch.Tensor, squeeze: bool, rs: int | None = None) -> torch.Tensor:
+    """A fresh output for a primitive whose kernel writes out[row * rs + m] with
+    the INPUT's row stride rs: allocated [N, H, rs] and viewed as [N, H, S], so a
+    strided input view (rs > S) gets an output of the same geometry."""
+    n, h, s = w3.shape
+    rs = s if rs is None else rs
+    out = torch.empty((n, h, rs), dtype=w3.dtype, device=w3.device)
+    if rs != s:
+        out = out[..., :s]
     return out[0] if squeeze else out
 
 
@@ -467,7 +474,7 @@ def _binary(name, op, a, b, width):
         b3, wb2, rs2 = _packed(b, width, "b")
         if b3.shape != a3.shape or wb2 != wb or rs2 != rs:
             raise ValueError("operands must have identical shape, dtype and stride")
-    o = _new_like(a3, squeeze)
+    o = _new_like(a3, squeeze, rs)
     o3 = _as3d(o, "out")
     n, h, _ = a3.shape
     _capi.call("be_bitop", op, _ptr(a3), _ptr(b3), _ptr(o3), wb, n, h,
@@ -491,7 +498,7 @@ def shift(words, width, direction: int, border=WHITE_OUTSIDE):
     """BitImage.shift (bitimage.py:207-240); direction BE_LEFT..BE_DOWN."""
     squeeze = words.dim() == 2
     w3, wb, rs = _packed(words, width)
-    o = _new_like(w3, squeeze)
+    o = _new_like(w3, squeeze, rs)
     n, h, _ = w3.shape
     _capi.call("be_shift", _ptr(w3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs, int(direction),
                fill_bit(border), _stream(w3))
@@ -505,7 +512,7 @@ def shift_and(img, mask, width, side: int, border=WHITE_OUTSIDE):
     m3, wb2, rs2 = _packed(mask, width, "mask")
     if m3.shape != i3.shape or wb2 != wb or rs2 != rs:
         raise ValueError("img and mask must have identical shape, dtype and stride")
-    o = _new_like(i3, squeeze)
+    o = _new_like(i3, squeeze, rs)
     n, h, _ = i3.shape
     _capi.call("be_shift_and", _ptr(i3), _ptr(m3), _ptr(_as3d(o, "out")), wb, n, h, int(width), rs,
                int(side), fill_bit(border), _stream(i3))
@@ -527,7 +534,7 @@ def scan_edges(words, width, border=WHITE_OUTSIDE, *, out=None):
     squeeze = words.dim() == 2
     w3, wb, rs = _packed(words, width)
     if out is None:
-        o = _new_like(w3, squeeze)
+        o = _new_like(w3, squeeze, rs)
     else:
         o = out
         if _row_stride(_check_out(o, w3, squeeze), "out") != rs:

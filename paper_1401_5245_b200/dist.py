@@ -8,7 +8,8 @@ with no distributed code; this layer is new.
 * Row sharding (config C4): rank r owns rows [lo, hi) of one giant raster;
   ranks 0 and G-1 use the border fill on their outer side (bitimage.py:216-223).
   `PeerHaloEdges`: the edge kernel reads the neighbours' boundary rows straight
-  from their HBM over NVLink (CUDA IPC peer pointers) -- one launch per step.
+  from their HBM over NVLink (CUDA IPC peer pointers) -- one launch per step,
+  ordered by a device-side step-counter handshake (stream memory operations).
   `RowShardedEdges`: one packed row to each row neighbour by grouped NCCL
   send/recv (8 KiB per message at 65536 px) while the interior rows, which need
   no halo, are computed; then the two boundary rows with the received halos.
@@ -56,6 +57,12 @@ def init(backend: str | None = None) -> tuple[int, int]:
     return rank, world
 
 
+def _needs_host_staging(t: torch.Tensor, group=None) -> bool:
+    """gloo has no CUDA send/recv: CUDA rows then travel through host copies
+    (the functional multi-rank tests on one GPU; NCCL moves them in HBM)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def exchange_halos(first_row: torch.Tensor, last_row: torch.Tensor, above: torch.Tensor,
                    below: torch.Tensor, rank: int, world: int, group=None):
     """Post the halo exchange of one row slab and return the pending works.
@@ -63,7 +70,20 @@ def exchange_halos(first_row: torch.Tensor, last_row: torch.Tensor, above: torch
     Sends `first_row` to rank-1 and `last_row` to rank+1; receives rank-1's
     last row into `above` and rank+1's first row into `below`.  At the image
     border (rank 0 above, rank world-1 below) nothing is exchanged and the
-    caller passes a NULL halo so the kernel applies the border fill."""
+    caller passes a NULL halo so the kernel applies the border fill.  Under
+    gloo, CUDA rows are staged through host memory and the exchange completes
+    before this returns (the returned list is then empty)."""
+    if world > 1 and _needs_host_staging(first_row, group):
+        h_first, h_last = first_row.cpu(), last_row.cpu()
+        h_above, h_below = torch.empty_like(h_first), torch.empty_like(h_last)
+        works = exchange_halos(h_first, h_last, h_above, h_below, rank, world, group)
+        for w in works:
+            w.wait()
+        if rank > 0:
+            above.copy_(h_above)
+        if rank < world - 1:
+            below.copy_(h_below)
+        return []
     ops = []
     if rank > 0:
         ops.append(dist.P2POp(dist.irecv, above, rank - 1, group))
@@ -114,7 +134,7 @@ class RowShardedEdges:
                                self.rank, self.world, self.group)
         above = self.above if self.rank > 0 else None
         below = self.below if self.rank < self.world - 1 else None
-        if not works:
+        if self.world == 1:
             self.compute(self.slab, None, None, self.out, 0, rows)
             return self.out
         if rows > 2:  # interior rows need no halo: overlap them with the exchange
@@ -127,17 +147,58 @@ class RowShardedEdges:
         return self.out
 
 
+# CUDA IPC mappings are per allocation and may be opened only once per process:
+# several exported buffers can live in one allocation (torch's caching
+# allocator), so opened bases are shared and reference-counted here
+_IPC_OPEN: dict = {}
+
+
+def _ipc_open(capi, ct, handle: bytes, off: int) -> int:
+    ent = _IPC_OPEN.get(handle)
+    if ent is None:
+        ptr = ct.c_void_p()
+        capi.call("be_ipc_open", ct.create_string_buffer(handle, 64), 0, ct.byref(ptr))
+        ent = _IPC_OPEN[handle] = [ptr.value, 0]
+    ent[1] += 1
+    return ent[0] + off
+
+
+def _ipc_release(capi, ct, handle: bytes) -> None:
+    ent = _IPC_OPEN.get(handle)
+    if ent is None:
+        return
+    ent[1] -= 1
+    if ent[1] == 0:
+        capi.call("be_ipc_close", ct.c_void_p(ent[0]), 0)
+        del _IPC_OPEN[handle]
+
+
 class PeerHaloEdges:
     """Row-sharded edges whose halo rows are read from the neighbour ranks'
     slabs over NVLink by the edge kernel itself (CUDA IPC peer pointers passed
-    as K3's `above` / `below`): no exchange step and one launch per step -- the
+    as K3's `above` / `below`): no exchange step and one kernel per step -- the
     fused alternative to `RowShardedEdges`' NCCL send/recv.
 
-    Setup exports this rank's slab (`be_ipc_export`), all-gathers the handles and
-    opens the row neighbours' (`be_ipc_open`).  Each step reads the neighbours'
-    boundary rows as they are in HBM at that moment, so the caller must make
-    every rank's slab complete before the step (a barrier after the producer;
-    the benchmark's slabs are written once before timing)."""
+    Setup exports this rank's slab and a small step-counter buffer
+    (`be_ipc_export`), all-gathers the handles and opens the row neighbours'
+    (`be_ipc_open`).  Every step runs a device-side producer -> consumer
+    handshake in stream order (`be_stream_write32` / `be_stream_wait_geq32`,
+    stream memory operations on the counters -- no host round trip, no
+    spinning kernel):
+
+        step():  ready[me] := s       this rank's slab of step s is complete
+                 wait ready[above] >= s and ready[below] >= s
+                 edge kernel (reads the neighbours' boundary rows)
+                 done[me] := s        finished reading the neighbours' rows
+
+        acquire_for_write():  wait done[above] >= s and done[below] >= s
+                 -- call before overwriting the slab for step s + 1, so no
+                 neighbour still reads step s's boundary rows.
+
+    The slab must be written on the current stream (or ordered before it)
+    before step()."""
+
+    READY, DONE = 0, 16          # counter word offsets (separate 64-byte lines)
 
     def __init__(self, slab: torch.Tensor, width: int, border=1, group=None):
         import ctypes
@@ -153,39 +214,78 @@ class PeerHaloEdges:
         self.slab, self.width, self.border = slab, int(width), border
         self.rows, self.stride = slab.shape[0], slab.stride(0)
         self.out = torch.empty_like(slab)
-        handle = (ctypes.c_char * 64)()
-        off = ctypes.c_int64()
-        _capi.call("be_ipc_export", ctypes.c_void_p(slab.data_ptr()), handle, ctypes.byref(off))
-        mine = (bytes(handle), off.value, self.rows, self.stride)
+        self.flags = torch.zeros(32, dtype=torch.int32, device=slab.device)
+        self.s = 0
+        torch.cuda.synchronize(slab.device)        # counters are zero before anyone waits
+        mine = (self._export(slab), self._export(self.flags), self.rows, self.stride)
         everyone = [None] * self.world
+        everyone[self.rank] = mine
         if self.world > 1:
             dist.all_gather_object(everyone, mine, group=group)
         self._opened = []
-        self.above_ptr = self._open(everyone[self.rank - 1], last_row=True) if self.rank > 0 else None
-        self.below_ptr = (self._open(everyone[self.rank + 1], last_row=False)
-                          if self.rank < self.world - 1 else None)
+        self.above_ptr = self.above_flags = self.below_ptr = self.below_flags = None
+        if self.rank > 0:
+            (h, off), (fh, foff), rows, stride = everyone[self.rank - 1]
+            self.above_ptr = self._open(h, off) + (rows - 1) * stride * 4
+            self.above_flags = self._open(fh, foff)
+        if self.rank < self.world - 1:
+            (h, off), (fh, foff), _, _ = everyone[self.rank + 1]
+            self.below_ptr = self._open(h, off)
+            self.below_flags = self._open(fh, foff)
 
-    def _open(self, info, last_row: bool) -> int:
+    def _export(self, t: torch.Tensor):
         ct = self._ct
-        handle, off, rows, stride = info
-        ptr = ct.c_void_p()
-        self._capi.call("be_ipc_open", ct.create_string_buffer(handle, 64), off, ct.byref(ptr))
-        self._opened.append((ptr.value, off))
-        return ptr.value + ((rows - 1) * stride * 4 if last_row else 0)
+        handle = (ct.c_char * 64)()
+        off = ct.c_int64()
+        self._capi.call("be_ipc_export", ct.c_void_p(t.data_ptr()), handle, ct.byref(off))
+        return bytes(handle), off.value
+
+    def _open(self, handle: bytes, off: int) -> int:
+        ptr = _ipc_open(self._capi, self._ct, handle, off)
+        self._opened.append(handle)
+        return ptr
+
+    def _stream(self):
+        return self._ct.c_void_p(torch.cuda.current_stream(self.slab.device).cuda_stream)
+
+    def _wait(self, flags_ptr, word, value, st):
+        if flags_ptr is not None:
+            self._capi.call("be_stream_wait_geq32", self._ct.c_void_p(flags_ptr + 4 * word),
+                            value, st)
+
+    def _publish(self, word, value, st):
+        self._capi.call("be_stream_write32", self._ct.c_void_p(self.flags.data_ptr() + 4 * word),
+                        value, st)
+
+    def acquire_for_write(self) -> None:
+        """Order the current stream after the neighbours' reads of this slab's
+        step-s boundary rows (call before rewriting the slab)."""
+        st = self._stream()
+        self._wait(self.above_flags, self.DONE, self.s, st)
+        self._wait(self.below_flags, self.DONE, self.s, st)
 
     def step(self) -> torch.Tensor:
         ct = self._ct
         from . import cuda as cu
 
+        self.s += 1
+        st = self._stream()
+        if self.world > 1:
+            self._publish(self.READY, self.s, st)
+            self._wait(self.above_flags, self.READY, self.s, st)
+            self._wait(self.below_flags, self.READY, self.s, st)
         self._capi.call("be_edge_packed_halo_u32", ct.c_void_p(self.slab.data_ptr()),
                         ct.c_void_p(self.above_ptr) if self.above_ptr else None,
                         ct.c_void_p(self.below_ptr) if self.below_ptr else None,
                         ct.c_void_p(self.out.data_ptr()), self.rows, self.width, self.stride,
-                        cu.fill_bit(self.border), 0, self.rows,
-                        ct.c_void_p(torch.cuda.current_stream().cuda_stream))
+                        cu.fill_bit(self.border), 0, self.rows, st)
+        if self.world > 1:
+            self._publish(self.DONE, self.s, st)
         return self.out
 
     def close(self):
-        for ptr, off in self._opened:
-            self._capi.call("be_ipc_close", self._ct.c_void_p(ptr), off)
+        """Unmap the neighbours' buffers (after every rank's last step has
+        finished reading, e.g. behind a barrier)."""
+        for h in self._opened:
+            _ipc_release(self._capi, self._ct, h)
         self._opened = []

@@ -28,7 +28,8 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Gpixel/s"
     assert d["higher_is_better"] is True and d["config"]["workload"]
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
+    assert cb["value"] == d["value"] and d["dtype"] == "u32"
     assert cb["host"]["cpu_count"] >= cb["cores"]
     assert d["e2e"] == {"value": d["value"], "unit": "Gpixel/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
@@ -43,9 +44,28 @@ def test_our_arm_line(cuda_dev):
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     cb = d["cpu_baseline"]
-    assert cb["cores"] == 1 and cb["kind"] == "port" and cb["value"] > 0 and cb["sample"]
+    assert cb["cores"] == 1 and cb["kind"] in ("reference", "port") and cb["value"] > 0
+    assert cb["sample"] and d["dtype"] == "u32"
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 256 * 256 and e["d2h_bytes_per_step"] == 256 * 8 * 4
     assert d["gpu_launches"] >= 2000
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
-    assert d["parity"]["ok"]
+    assert d["parity"]["ok"] and d["parity"]["checked_px"] == 256 * 256
+    assert d["e2e"]["dropin"]["per_call_us"] > 0
+
+
+def test_both_arms_share_config():
+    """The driver compares the two arms' `config` dicts: one function makes both."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert b.DEFAULT_CONFIG == "c4"
+    for cfg in b.CONFIGS:
+        for world in (1, 2, 8):
+            c = b.workload_config(cfg, world, False)
+            assert c == b.workload_config(cfg, world, False) and c["config_id"] == cfg
+    ref = _run("--impl", "reference", "--config", "c2", "--steps", "2", "--warmup", "1")
+    assert ref["config"] == b.workload_config("c2", 1, False)
+    assert ref["cpu_baseline"]["sample"].startswith("the whole config every step (16777216 px")

@@ -24,25 +24,34 @@ def _port():
 
 
 @pytest.mark.parametrize("extra", [["--config", "c2", "--steps", "300"],
+                                   ["--config", "c2", "--steps", "300", "--weak"],
                                    ["--config", "c4", "--steps", "4"],
-                                   ["--config", "c4", "--steps", "4", "--no-e2e", "--halo", "nccl"]],
-                         ids=["c2-batch", "c4-rows-p2p", "c4-rows-nccl"])
+                                   ["--config", "c4", "--steps", "4", "--halo", "p2p"]],
+                         ids=["c2-strong", "c2-weak", "c4-rows-nccl-path", "c4-rows-p2p"])
 def test_bench_two_ranks_one_gpu(extra, cuda_dev):
-    if "nccl" in extra:
-        pytest.skip("NCCL halos need two devices (gloo has no CUDA send/recv)")
+    """The NCCL halo path runs RowShardedEdges on CUDA with gloo standing in for
+    NCCL (rows staged through the host); p2p runs the IPC peer reads with the
+    device-side handshake."""
     env = dict(os.environ, BITEDGE_SHARE_GPU="1", BITEDGE_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--warmup", "3", *extra]
-    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+           "--warmup", "3", "--no-dropin", *extra]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stderr[-2000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, res.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["parity"]["ok"]
+    assert d["parity"]["ranks"] == 2
     if "c4" in extra:
-        assert d["scaling"] == "strong" and "p2p" in d["config"]["parallelism"]
+        assert d["scaling"] == "strong" and "row-shard x2" in d["config"]["parallelism"]
+        assert ("p2p" if "p2p" in extra else "nccl") in d["method"]["halo"]
+        assert "per-iteration barrier" in d["method"]["timing"]
+        assert d["parity"]["checked_px"] == 65536 * 65536
         # e2e of the row shards (host halos): both ranks' slabs plus their halo rows
         assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > (65536 * 2048 * 4)
-    else:
+    elif "--weak" in extra:
         assert d["scaling"] == "weak" and d["config"]["global_batch"] == 8192
+    else:
+        assert d["scaling"] == "strong" and d["config"]["global_batch"] == 4096
+        assert d["parity"]["checked_px"] == 4096 * 64 * 64

@@ -1,8 +1,9 @@
-"""Peer-memory halos (PeerHaloEdges): two ranks on ONE GPU exchange CUDA IPC
-handles over gloo and each runs a single edge kernel that reads its
-neighbour's boundary row straight from the other process's allocation.  No
-kernel waits on another (the slabs are written before a barrier), so sharing
-one device is safe; on an 8-GPU box the same pointers resolve over NVLink."""
+"""Peer-memory halos (PeerHaloEdges): two or three ranks on ONE GPU exchange
+CUDA IPC handles over gloo and each runs a single edge kernel that reads its
+neighbour's boundary row straight from the other process's allocation; on an
+8-GPU box the same pointers resolve over NVLink.  No kernel waits on another:
+the per-step handshake is stream memory operations on IPC-shared counters,
+which the GPU front end resolves (a blocked stream holds no SM)."""
 
 import os
 import socket
@@ -60,3 +61,56 @@ def test_peer_halo_two_processes_one_gpu(world, cuda_dev):
     q = ctx.Queue()
     mp.spawn(_worker, args=(world, _port(), 150, 8192, q), nprocs=world, join=True)
     assert q.get(timeout=120) is True
+
+
+def _worker_rewrite(rank, world, port, H, W, steps, q):
+    """Slabs REWRITTEN every step, with skewed producers: step k's raster is
+    fresh random bits; before writing, odd ranks stall their stream on even
+    steps and even ranks on odd steps (torch.cuda._sleep), so without the
+    handshake a neighbour would read the previous step's boundary rows (or a
+    half-written slab)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import cscan
+        from oracle import port as P
+        from paper_1401_5245_b200.dist import PeerHaloEdges, shard_range
+
+        lo, hi = shard_range(H, rank, world)
+        rasters = []
+        for k in range(steps):
+            img = (np.random.default_rng([7, k]).random((H, W)) < 0.5).astype(np.uint8)
+            rasters.append(P.pack_u32(img))
+        src = torch.from_numpy(np.stack([r[lo:hi] for r in rasters]).view(np.int32)).cuda()
+        slab = torch.zeros_like(src[0])
+        torch.cuda.synchronize()
+        ph = PeerHaloEdges(slab, W, 1)
+        dist.barrier()
+        outs = []
+        for k in range(steps):
+            ph.acquire_for_write()              # neighbours are done with step k-1's rows
+            if (k + rank) % 2 == 0:
+                torch.cuda._sleep(2_000_000)    # ~1 ms stall before this producer writes
+            slab.copy_(src[k])
+            outs.append(ph.step().clone())
+        torch.cuda.synchronize()
+        ok = True
+        for k in range(steps):
+            exp = cscan.scan_p32(rasters[k], W, 1)[lo:hi]
+            ok &= bool((outs[k].cpu().numpy().view(np.uint32) == exp).all())
+        dist.barrier()
+        ph.close()
+        res = [None] * world
+        dist.all_gather_object(res, ok)
+        if rank == 0:
+            q.put(all(res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_halo_handshake_rewritten_slabs(world, cuda_dev):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker_rewrite, args=(world, _port(), 96, 4096, 12, q), nprocs=world, join=True)
+    assert q.get(timeout=180) is True
