@@ -236,6 +236,19 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
                        int emit_edgeset, uint8_t *dev_pix_or_null, uint64_t *dev_packed_or_null,
                        uint64_t *dev_out_or_null, uint64_t *host_out, void *stream);
 
+/* The same one-call flow for SMALL images from ANY host memory (the drop-in's
+ * per-image hot path, C1/C2-sized rasters): the pixels (row stride
+ * pix_row_stride bytes, need not be page-locked) are copied into the caller's
+ * page-locked staging buffer stage_in (>= h*w bytes), ONE kernel reads them and
+ * writes the uint64 words into page-locked stage_out (>= h*ceil(w/64)*8 bytes)
+ * over PCIe, and after the stream drains the words are copied to words_out (any
+ * host memory).  w < 1024.  The staging buffers are reusable as soon as the call
+ * returns (one pair per calling thread keeps the page-locked footprint fixed). */
+int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_t h, int64_t w,
+                              int fill_bit, int emit_edgeset, uint8_t *stage_in,
+                              int64_t stage_in_bytes, uint64_t *stage_out,
+                              int64_t stage_out_bytes, uint64_t *words_out, void *stream);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);
 int be_abi_version(void);

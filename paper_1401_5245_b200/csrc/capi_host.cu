@@ -195,6 +195,43 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
     return BE_OK;
 }
 
+int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_t h, int64_t w,
+                              int fill_bit, int emit_edgeset, uint8_t *stage_in,
+                              int64_t stage_in_bytes, uint64_t *stage_out,
+                              int64_t stage_out_bytes, uint64_t *words_out, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, 64, 1, h, w, fill_bit);
+    if (rc) return rc;
+    if (!pix || !stage_in || !stage_out || !words_out)
+        return fail(BE_EINVAL, "buffers must not be NULL");
+    if (w >= 1024) return fail(BE_EINVAL, "the staged zero-copy flow needs w < 1024");
+    if (pix_row_stride < w) return fail(BE_EINVAL, "pixel row stride < width");
+    const int64_t wp = G.wp / 2;                                 // uint64 words per row
+    if (h * w > stage_in_bytes || h * wp * 8 > stage_out_bytes)
+        return fail(BE_EINVAL, "staging buffers too small for a %lldx%lld image",
+                    (long long)w, (long long)h);
+    // the caller's pixels (any host memory) into the page-locked staging buffer
+    if (pix_row_stride == w) {
+        memcpy(stage_in, pix, (size_t)(h * w));
+    } else {
+        for (int64_t y = 0; y < h; ++y)
+            memcpy(stage_in + y * w, pix + y * pix_row_stride, (size_t)w);
+    }
+    cudaStream_t st = S(stream);
+    uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t *dst = (uint32_t *)stage_out;
+    // one launch reading / writing the mapped page-locked buffers over PCIe:
+    // pack (bitimage.py:122-136) + edges, uint64 words
+    rc = edges_impl(stage_in, 1, w, nullptr, nullptr, emit_edgeset ? nullptr : dst,
+                    emit_edgeset ? dst : nullptr, side, nullptr, 64, wp, 1, h, w, fill_bit, 0, h,
+                    st);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    memcpy(words_out, stage_out, (size_t)(h * wp * 8));
+    return BE_OK;
+}
+
 int be_host_edges_rows(const void *host_in, int input_kind, uint32_t *host_out, int64_t h,
                        int64_t w, int fill_bit, int halo_flags, void *const dev_in[2],
                        uint32_t *const dev_out[2], int64_t chunk_rows, void *stream0,

@@ -16,6 +16,7 @@ bool [N, H, W] (any nonzero byte is white, bitimage.py:124, 133).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -256,6 +257,52 @@ def host_detect(host_pixels: torch.Tensor, border=WHITE_OUTSIDE, *, edgeset: boo
     words = host.numpy().view(np.uint64)
     words.setflags(write=False)
     return out, packed, words
+
+
+# the drop-in's small-image flow (be_host_detect_u64_staged): one page-locked
+# staging pair per calling thread, reused by every call -- a fixed pinned
+# footprint however many images are in flight in Python
+SMALL_MAX_PIXELS = 1 << 20
+_tls = threading.local()
+
+
+def _staging(in_bytes: int, out_bytes: int):
+    st = getattr(_tls, "stage", None)
+    if st is None or st[0].numel() < in_bytes or st[1].numel() < out_bytes:
+        old_in = 0 if st is None else st[0].numel()
+        old_out = 0 if st is None else st[1].numel()
+        st = (torch.empty(max(in_bytes, old_in, 64 << 10), dtype=torch.uint8, pin_memory=True),
+              torch.empty(max(out_bytes, old_out, 16 << 10), dtype=torch.uint8, pin_memory=True))
+        _tls.stage = st
+    return st
+
+
+def host_detect_small(pix: np.ndarray, border=WHITE_OUTSIDE, *, edgeset: bool = False,
+                      device_index: int | None = None) -> np.ndarray:
+    """`detect_edges_mask(BitImage.from_array(a)).words` for a small host image
+    in ONE native call (`be_host_detect_u64_staged`): uint8 pixels [H, W] in any
+    host memory (nonzero = white; W < 1024, H*W <= SMALL_MAX_PIXELS) -> a fresh
+    read-only uint64 words array [H, ceil(W/64)].  The pixels go through this
+    thread's page-locked staging pair; one kernel packs and detects reading and
+    writing them over PCIe."""
+    if pix.ndim != 2 or pix.dtype != np.uint8 or pix.strides[1] != 1:
+        raise ValueError("pix must be a uint8 [H, W] array with contiguous rows")
+    h, w = pix.shape
+    wp = -(-w // 64)
+    if w >= 1024 or h * w > SMALL_MAX_PIXELS:
+        raise ValueError("host_detect_small takes images narrower than 1024 px, <= 1 Mpx")
+    stage_in, stage_out = _staging(h * w, h * wp * 8)
+    words = np.empty((h, wp), dtype=np.uint64)
+    dev = torch.cuda.current_device() if device_index is None else device_index
+    rc = _capi.fn("be_host_detect_u64_staged")(
+        pix.ctypes.data, pix.strides[0], h, w, fill_bit(border), 1 if edgeset else 0,
+        stage_in.data_ptr(), stage_in.numel(), stage_out.data_ptr(), stage_out.numel(),
+        words.ctypes.data, _raw_stream(dev) if _raw_stream is not None
+        else torch.cuda.current_stream(dev).cuda_stream)
+    if rc:
+        _capi.check(rc)
+    words.setflags(write=False)
+    return words
 
 
 def _pixels(pixels: torch.Tensor, what="pixels"):

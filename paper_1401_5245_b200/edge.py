@@ -56,12 +56,20 @@ def fundamental_edge(img: BitImage, mask: BitImage, side: Direction,
 
 def _edges(img: BitImage, border: BorderPolicy, edgeset: bool) -> BitImage:
     pix = img._take_pixels()
+    if pix is not None and not hasattr(pix, "t"):
+        # small host image, nothing uploaded yet: pack + edges in one kernel over
+        # the thread's page-locked staging pair, words back, in one native call;
+        # the result holds host words (uploaded on demand), the input keeps its
+        # pixels (packed on demand)
+        res = BitImage._wrap(img.width, img.height, None)
+        res._words = _cuda().host_detect_small(pix, border.fill_bit, edgeset=edgeset)
+        return res
     if pix is not None:
-        # from_array of a host array, nothing uploaded yet: upload, pack + edges
-        # (one launch) and the result's download in one native call; the result
-        # holds its words on the host (and in HBM when the call staged them
+        # from_array of a larger host array, nothing uploaded yet: upload, pack +
+        # edges (one launch) and the result's download in one native call; the
+        # result holds its words on the host (and in HBM when the call staged them
         # there), the input keeps its packed words in HBM
-        out, packed, host = _cuda().host_detect(pix, border.fill_bit, edgeset=edgeset)
+        out, packed, host = _cuda().host_detect(pix.t, border.fill_bit, edgeset=edgeset)
         img._adopt_packed(packed)
         res = BitImage._wrap(img.width, img.height, out)   # out None: uploaded on demand
         res._words = host

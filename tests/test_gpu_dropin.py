@@ -1,7 +1,8 @@
 """The drop-in BitImage's deferred pack: `from_array` on a host array keeps a
-page-locked copy of the pixels; detect_edges_mask / edge_set run upload, pack +
-edges and the result's download as one call (and leave the packed words
-behind), every other consumer uploads and packs first.  All results
+private copy of the pixels (pageable for small images, page-locked within a
+budget for larger ones); detect_edges_mask / edge_set run upload, pack + edges
+and the result's download as one call (the larger flow also leaves the packed
+words behind), every other consumer uploads and packs first.  All results
 word-identical to the reference composition (oracle/port.py)."""
 
 import numpy as np
@@ -28,8 +29,12 @@ def test_fused_pack_then_words(policy, cuda_dev):
         ref = P.from_array(a)
         img = BitImage.from_array(a)
         assert img._pix is not None                          # deferred
+        small = w < 1024 and h * w <= (1 << 20)
         e = detect_edges_mask(img, b)
-        assert img._pix is None and img._dev is not None     # packed by the same launch
+        if small:       # staged one-call flow: nothing left on the device
+            assert isinstance(img._pix, np.ndarray) and img._dev is None
+        else:
+            assert img._pix is None and img._dev is not None     # packed by the same launch
         assert (e.words == P.detect_edges_mask(ref, b.value).words).all()
         assert (img.words == ref.words).all()
         img2 = BitImage.from_array(a)
@@ -279,3 +284,75 @@ def test_host_detect_refuses_pageable_zero_copy(cuda_dev):
     rc = _capi.fn("be_host_detect_u64")(hp.data_ptr(), h, w, 1, 0, None, pk.data_ptr(), None,
                                         out.ctypes.data, None)
     assert rc < 0
+
+
+def test_small_flow_input_forms(cuda_dev):
+    """The staged small-image flow on non-contiguous, reversed, bool and int
+    arrays, and the caller mutating its array after from_array."""
+    from paper_1401_5245_b200.bitimage import BitImage
+    from paper_1401_5245_b200.edge import detect_edges_mask, edge_set
+
+    base = _img(11, 80, 300)
+    for a in (base[:, ::-1], base[::2, 5:250], base.astype(bool), base.astype(np.int32) * -3,
+              np.asfortranarray(base), base[::-1]):
+        ref = P.from_array(a)
+        img = BitImage.from_array(a)
+        assert (detect_edges_mask(img).words == P.detect_edges_mask(ref).words).all()
+        assert (edge_set(img).words == P.edge_set(ref).words).all()
+        assert (img.words == ref.words).all()
+    a = base.copy()
+    img = BitImage.from_array(a)
+    a[:] = 0                                                  # private copy: unaffected
+    ref = P.from_array(base)
+    assert (detect_edges_mask(img).words == P.detect_edges_mask(ref).words).all()
+
+
+def test_pinned_budget_bounds_pending_copies(cuda_dev, monkeypatch):
+    """Pending page-locked copies never exceed the budget: past it, from_array
+    uploads and packs at once; the held bytes return to zero as images go."""
+    import gc
+
+    from paper_1401_5245_b200 import bitimage as B
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    monkeypatch.setattr(B, "_PINNED_BUDGET", 3 * 1200 * 1100)
+    gc.collect()
+    held0 = B._pinned_held[0]
+    a = _img(12, 1200, 1100)                  # > 1 Mpx: the page-locked flow
+    ref = P.from_array(a)
+    imgs = [B.BitImage.from_array(a) for _ in range(5)]
+    pending = [i for i in imgs if i._pix is not None]
+    assert len(pending) == 3 and all(i._dev is not None for i in imgs[3:])
+    assert B._pinned_held[0] - held0 == 3 * 1200 * 1100
+    for i in imgs:
+        assert (detect_edges_mask(i).words == P.detect_edges_mask(ref).words).all()
+        assert (i.words == ref.words).all()
+    del imgs, pending, i
+    gc.collect()
+    assert B._pinned_held[0] == held0
+
+
+def test_small_flow_from_threads(cuda_dev):
+    """Per-thread staging: eight threads running the one-call flow at once."""
+    import threading
+
+    from paper_1401_5245_b200.bitimage import BitImage
+    from paper_1401_5245_b200.edge import detect_edges_mask
+
+    errors = []
+
+    def worker(k):
+        try:
+            for it in range(40):
+                a = _img(1000 * k + it, 20 + it, 64 + 7 * k)
+                got = detect_edges_mask(BitImage.from_array(a)).words
+                assert (got == P.detect_edges_mask(P.from_array(a)).words).all()
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
