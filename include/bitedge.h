@@ -242,12 +242,15 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
  * page-locked staging buffer stage_in (>= h*w bytes), ONE kernel reads them and
  * writes the uint64 words into page-locked stage_out (>= h*ceil(w/64)*8 bytes)
  * over PCIe, and after the stream drains the words are copied to words_out (any
- * host memory).  w < 1024.  The staging buffers are reusable as soon as the call
+ * host memory).  With dev_stage_or_null (>= h*w bytes of device memory) the
+ * pixels cross PCIe by one copy-engine transfer into it instead and the kernel
+ * reads HBM (faster past a few tens of KB).  w < 1024.  The staging buffers are reusable as soon as the call
  * returns (one pair per calling thread keeps the page-locked footprint fixed). */
 int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_t h, int64_t w,
                               int fill_bit, int emit_edgeset, uint8_t *stage_in,
                               int64_t stage_in_bytes, uint64_t *stage_out,
-                              int64_t stage_out_bytes, uint64_t *words_out, void *stream);
+                              int64_t stage_out_bytes, uint8_t *dev_stage_or_null,
+                              uint64_t *words_out, void *stream);
 
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);

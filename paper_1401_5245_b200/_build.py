@@ -21,6 +21,35 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
+EXT_SRC = "dropin_ext.c"
+
+
+def ext_path() -> str:
+    import sysconfig
+
+    return os.path.join(HERE, "_dropin" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_ext() -> str:
+    """The CPython binding of the drop-in's per-image call (csrc/dropin_ext.c),
+    linked against the library (rpath $ORIGIN/lib)."""
+    import sysconfig
+
+    import numpy
+
+    out = ext_path()
+    tmp = out + ".tmp"
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-std=c11",
+           "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(),
+           os.path.join(CSRC, EXT_SRC), "-L", LIB_DIR, "-lbitedge_cuda",
+           "-Wl,-rpath,$ORIGIN/lib", "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"extension build failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):
@@ -29,10 +58,10 @@ def nvcc() -> str:
 
 
 def _stale() -> bool:
-    if not os.path.exists(LIB_PATH):
+    if not os.path.exists(LIB_PATH) or not os.path.exists(ext_path()):
         return True
-    t = os.path.getmtime(LIB_PATH)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    t = min(os.path.getmtime(LIB_PATH), os.path.getmtime(ext_path()))
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS + [EXT_SRC]]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -65,6 +94,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.replace(tmp, LIB_PATH)
     finally:
         shutil.rmtree(tmpdir, ignore_errors=True)
+    build_ext()
     log = "".join(err for _, err in results)
     if verbose:
         print(log)

@@ -59,7 +59,8 @@ _SIGNATURES = {
     "be_host_edges_rows": [_P, _INT, _P, _I64, _I64, _INT, _INT, ctypes.POINTER(_P),
                            ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_host_detect_u64": [_P, _I64, _I64, _INT, _INT, _P, _P, _P, _P, _P],
-    "be_host_detect_u64_staged": [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _P, _P],
+    "be_host_detect_u64_staged": [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _P, _P,
+                                  _P],
     "be_last_error": [],
     "be_abi_version": [],
     "be_launch_count": [],

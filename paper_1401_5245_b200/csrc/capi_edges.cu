@@ -129,18 +129,18 @@ int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
             return kNoKernel;
         } else {
             // widest alignment every row start has (rp.v8 carries it: 8, 4 or 1)
-            if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, 0, st, rp);
-            else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, 0, st, rp);
-            else launch_k(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, 0, st, rp);
+            if (rp.v8 == 8) launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, u8_block(), 0, st, rp);
+            else if (rp.v8 == 4) launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, u8_block(), 0, st, rp);
+            else launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, u8_block(), 0, st, rp);
             return cuda_check("edge_reg_u8_kernel<UNAL>");
         }
     }
     if (rp.v8) {
-        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, 0, st, rp);
-        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, 0, st, rp);
+        if (rs == 8) launch_kb(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, u8_block(), 0, st, rp);
+        else launch_kb(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, u8_block(), 0, st, rp);
     } else {
-        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, 0, st, rp);
-        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, 0, st, rp);
+        if (rs == 8) launch_kb(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, u8_block(), 0, st, rp);
+        else launch_kb(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, u8_block(), 0, st, rp);
     }
     return cuda_check("edge_reg_u8_kernel");
 }
@@ -436,7 +436,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     if (rp.in_end && getenv("BITEDGE_UNAL_RS4")) rs = 4;
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
-    const int64_t grid = (threads + kThreads - 1) / kThreads;
+    // K2 on zero-copy host input takes the caller's (smaller) block size
+    const int64_t blk = (input_kind == 1 && !multi_out(rp)) ? u8_block() : kThreads;
+    const int64_t grid = (threads + blk - 1) / blk;
     if (grid > 0x7FFFFFFFLL) return kNoKernel;
     if (above || below)
         return launch_reg_halo<true>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);

@@ -3,6 +3,8 @@
 // only state: a thread-local error string and launch counter.
 #include "capi_internal.cuh"
 
+#include <time.h>
+
 using namespace bitedge;
 using namespace bitedge::capi;
 
@@ -10,6 +12,7 @@ namespace bitedge {
 namespace capi {
 thread_local char g_err[512];
 thread_local int64_t g_launches = 0;
+thread_local int g_u8_block = 0;
 }  // namespace capi
 }  // namespace bitedge
 
@@ -198,7 +201,8 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
 int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_t h, int64_t w,
                               int fill_bit, int emit_edgeset, uint8_t *stage_in,
                               int64_t stage_in_bytes, uint64_t *stage_out,
-                              int64_t stage_out_bytes, uint64_t *words_out, void *stream) {
+                              int64_t stage_out_bytes, uint8_t *dev_stage_or_null,
+                              uint64_t *words_out, void *stream) {
     Geometry G;
     int rc = make_geometry(G, 64, 1, h, w, fill_bit);
     if (rc) return rc;
@@ -210,6 +214,10 @@ int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_
     if (h * w > stage_in_bytes || h * wp * 8 > stage_out_bytes)
         return fail(BE_EINVAL, "staging buffers too small for a %lldx%lld image",
                     (long long)w, (long long)h);
+    // BITEDGE_TRACE_STAGED=1 (experiments): per-phase host time, printed every 2000 calls
+    static const bool trace = getenv("BITEDGE_TRACE_STAGED") != nullptr;
+    struct timespec ts[5];
+    if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[0]);
     // the caller's pixels (any host memory) into the page-locked staging buffer
     if (pix_row_stride == w) {
         memcpy(stage_in, pix, (size_t)(h * w));
@@ -217,18 +225,73 @@ int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_
         for (int64_t y = 0; y < h; ++y)
             memcpy(stage_in + y * w, pix + y * pix_row_stride, (size_t)w);
     }
+    if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[1]);
     cudaStream_t st = S(stream);
     uint32_t *side[4] = {nullptr, nullptr, nullptr, nullptr};
     uint32_t *dst = (uint32_t *)stage_out;
-    // one launch reading / writing the mapped page-locked buffers over PCIe:
+    const uint8_t *src = stage_in;
+    if (dev_stage_or_null) {
+        // larger images: one copy-engine transfer (large PCIe requests) into HBM
+        cudaError_t e = cudaMemcpyAsync(dev_stage_or_null, stage_in, (size_t)(h * w),
+                                        cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return fail((int)e, "H2D: %s", cudaGetErrorString(e));
+        src = dev_stage_or_null;
+    }
+    // one launch reading the pixels (mapped page-locked staging over PCIe, or
+    // HBM) and writing the words into the mapped page-locked staging buffer:
     // pack (bitimage.py:122-136) + edges, uint64 words
-    rc = edges_impl(stage_in, 1, w, nullptr, nullptr, emit_edgeset ? nullptr : dst,
+    static const int zc_block = [] {
+        const char *e = getenv("BITEDGE_ZC_BLOCK");       // experiments: 32..256
+        return e ? atoi(e) : 0;
+    }();
+    if (!dev_stage_or_null) g_u8_block = zc_block;
+    rc = edges_impl(src, 1, w, nullptr, nullptr, emit_edgeset ? nullptr : dst,
                     emit_edgeset ? dst : nullptr, side, nullptr, 64, wp, 1, h, w, fill_bit, 0, h,
                     st);
+    g_u8_block = 0;
     if (rc) return rc;
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[2]);
+    // completion: BITEDGE_STAGED_SPIN=1 (experiments) enqueues a stream write of a
+    // per-thread sequence number into page-locked memory after the kernel and
+    // spins on it; otherwise cudaStreamSynchronize
+    static const bool spin = getenv("BITEDGE_STAGED_SPIN") != nullptr;
+    static thread_local uint32_t seq = 0;
+    uint32_t *flag = (uint32_t *)((char *)stage_out + ((stage_out_bytes - 64) & ~(int64_t)63));
+    cudaError_t e = cudaSuccess;
+    if (spin && stage_out_bytes - 64 >= h * wp * 8) {
+        ++seq;
+        rc = be_stream_write32(flag, seq, stream);
+        if (rc) return rc;
+        for (uint64_t i = 1;; ++i) {
+            if (*(volatile uint32_t *)flag == seq) break;
+            if ((i & 4095) == 0 && (e = cudaStreamQuery(st)) != cudaErrorNotReady) {
+                if (e != cudaSuccess) break;
+                if (*(volatile uint32_t *)flag == seq) break;
+            }
+        }
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+            return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    } else {
+        e = cudaStreamSynchronize(st);
+    }
+    if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[3]);
     memcpy(words_out, stage_out, (size_t)(h * wp * 8));
+    if (trace) {
+        clock_gettime(CLOCK_MONOTONIC, &ts[4]);
+        static thread_local double acc[4];
+        static thread_local int calls;
+        for (int i = 0; i < 4; ++i)
+            acc[i] += (ts[i + 1].tv_sec - ts[i].tv_sec) * 1e6 + (ts[i + 1].tv_nsec - ts[i].tv_nsec) * 1e-3;
+        if (++calls == 2000) {
+            fprintf(stderr, "[staged %lldx%lld] memcpy_in %.2f  launch %.2f  sync %.2f  memcpy_out %.2f us\n",
+                    (long long)w, (long long)h, acc[0] / calls, acc[1] / calls, acc[2] / calls,
+                    acc[3] / calls);
+            calls = 0;
+            for (int i = 0; i < 4; ++i) acc[i] = 0;
+        }
+    }
     return BE_OK;
 }
 

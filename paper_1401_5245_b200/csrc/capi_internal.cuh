@@ -17,9 +17,15 @@
 namespace bitedge {
 namespace capi {
 
-// the only state: this thread's error text and launch counter (capi_host.cu)
+// the only state: this thread's error text and launch counter (capi_host.cu),
+// and the block size K2 uses for the call in progress (set by the zero-copy
+// host flows, whose kernels read pinned host memory: smaller CTAs spread the
+// PCIe reads over more SMs; 0 = kThreads)
 extern thread_local char g_err[512];
 extern thread_local int64_t g_launches;
+extern thread_local int g_u8_block;
+
+inline unsigned u8_block() { return g_u8_block > 0 ? (unsigned)g_u8_block : (unsigned)kThreads; }
 
 inline int fail(int code, const char *fmt, ...) {
     va_list ap;

@@ -16,6 +16,7 @@ bool [N, H, W] (any nonzero byte is white, bitimage.py:124, 133).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -260,48 +261,113 @@ def host_detect(host_pixels: torch.Tensor, border=WHITE_OUTSIDE, *, edgeset: boo
 
 
 # the drop-in's small-image flow (be_host_detect_u64_staged): one page-locked
-# staging pair per calling thread, reused by every call -- a fixed pinned
-# footprint however many images are in flight in Python
+# staging pair (plus one device staging buffer) per calling thread, reused by
+# every call -- a fixed footprint however many images are in flight in Python
 SMALL_MAX_PIXELS = 1 << 20
+# from this many pixels on, the pixels cross PCIe by one copy-engine transfer
+# instead of being read by the kernel from mapped memory (scripts/dropin_breakdown.py)
+DEV_STAGE_MIN_PIXELS = int(os.environ.get("BITEDGE_DEV_STAGE_MIN", 1 << 40))
 _tls = threading.local()
+_staged_fn = None
+_get_device = getattr(torch._C, "_cuda_getDevice", None)
 
 
-def _staging(in_bytes: int, out_bytes: int):
+class _Stage:
+    __slots__ = ("pin_in", "pin_out", "dev", "in_ptr", "in_n", "out_ptr", "out_n", "dev_ptr",
+                 "dev_n", "device")
+
+    def __init__(self, in_bytes, out_bytes, dev_bytes, device):
+        self.pin_in = torch.empty(in_bytes, dtype=torch.uint8, pin_memory=True)
+        self.pin_out = torch.empty(out_bytes, dtype=torch.uint8, pin_memory=True)
+        self.dev = torch.empty(max(1, dev_bytes), dtype=torch.uint8,
+                               device=torch.device("cuda", device))
+        self.in_ptr, self.in_n = self.pin_in.data_ptr(), in_bytes
+        self.out_ptr, self.out_n = self.pin_out.data_ptr(), out_bytes
+        self.dev_ptr, self.dev_n = self.dev.data_ptr(), dev_bytes
+        self.device = device
+
+
+def _staging(in_bytes: int, out_bytes: int, device: int, dev_bytes: int = 0) -> _Stage:
     st = getattr(_tls, "stage", None)
-    if st is None or st[0].numel() < in_bytes or st[1].numel() < out_bytes:
-        old_in = 0 if st is None else st[0].numel()
-        old_out = 0 if st is None else st[1].numel()
-        st = (torch.empty(max(in_bytes, old_in, 64 << 10), dtype=torch.uint8, pin_memory=True),
-              torch.empty(max(out_bytes, old_out, 16 << 10), dtype=torch.uint8, pin_memory=True))
+    if st is None or st.device != device or st.in_n < in_bytes or st.out_n < out_bytes or \
+            st.dev_n < dev_bytes:
+        keep = (0, 0, 0) if st is None or st.device != device else (st.in_n, st.out_n, st.dev_n)
+        st = _Stage(max(in_bytes, keep[0], 64 << 10), max(out_bytes, keep[1], 16 << 10),
+                    max(dev_bytes, keep[2]), device)
         _tls.stage = st
     return st
 
 
-def host_detect_small(pix: np.ndarray, border=WHITE_OUTSIDE, *, edgeset: bool = False,
-                      device_index: int | None = None) -> np.ndarray:
+try:  # CPython binding of the same call (csrc/dropin_ext.c): ~4 us less per call
+    from . import _dropin
+except ImportError:  # pragma: no cover - the ctypes path below runs the same kernel
+    _dropin = None
+
+
+def _dropin_stage(in_bytes: int, out_bytes: int, device: int) -> None:
+    """(Re)allocate this thread's staging pair + private stream and register it
+    with the CPython binding."""
+    st = getattr(_tls, "ext_stage", None)
+    if st is not None and st[5] == device:
+        in_bytes, out_bytes = max(in_bytes, st[1]), max(out_bytes, st[3])
+    pin_in = torch.empty(max(in_bytes, 64 << 10), dtype=torch.uint8, pin_memory=True)
+    pin_out = torch.empty(max(out_bytes, 16 << 10), dtype=torch.uint8, pin_memory=True)
+    stream = torch.cuda.Stream(torch.device("cuda", device))
+    _tls.ext_stage = (pin_in, pin_in.numel(), pin_out, pin_out.numel(), stream, device)
+    _dropin.set_stage(pin_in.data_ptr(), pin_in.numel(), pin_out.data_ptr(), pin_out.numel(),
+                      stream.cuda_stream, device)
+
+
+def host_detect_small(pix: np.ndarray, border=WHITE_OUTSIDE, *, edgeset: bool = False) -> np.ndarray:
     """`detect_edges_mask(BitImage.from_array(a)).words` for a small host image
     in ONE native call (`be_host_detect_u64_staged`): uint8 pixels [H, W] in any
     host memory (nonzero = white; W < 1024, H*W <= SMALL_MAX_PIXELS) -> a fresh
     read-only uint64 words array [H, ceil(W/64)].  The pixels go through this
-    thread's page-locked staging pair; one kernel packs and detects reading and
-    writing them over PCIe."""
+    thread's page-locked staging pair; one kernel packs and detects, reading the
+    pixels over PCIe (or from HBM after one copy-engine transfer, for images of
+    DEV_STAGE_MIN_PIXELS and more) and writing the words into the staging pair."""
+    global _staged_fn
+    if _dropin is not None:
+        fb = getattr(border, "value", border)
+        if fb != 0 and fb != 1:
+            fb = fill_bit(border)
+        dev = _get_device() if _get_device is not None else torch.cuda.current_device()
+        es = 1 if edgeset else 0
+        r = _dropin.detect_small(pix, fb, es, dev)
+        if r is None:
+            h, w = pix.shape
+            if w >= 1024 or h * w > SMALL_MAX_PIXELS:
+                raise ValueError("host_detect_small takes images narrower than 1024 px, <= 1 Mpx")
+            _dropin_stage(h * w, h * ((w + 63) >> 6) * 8 + 128, dev)
+            r = _dropin.detect_small(pix, fb, es, dev)
+        return r
     if pix.ndim != 2 or pix.dtype != np.uint8 or pix.strides[1] != 1:
         raise ValueError("pix must be a uint8 [H, W] array with contiguous rows")
     h, w = pix.shape
-    wp = -(-w // 64)
     if w >= 1024 or h * w > SMALL_MAX_PIXELS:
         raise ValueError("host_detect_small takes images narrower than 1024 px, <= 1 Mpx")
-    stage_in, stage_out = _staging(h * w, h * wp * 8)
+    fb = getattr(border, "value", border)
+    if fb != 0 and fb != 1:
+        fb = fill_bit(border)
+    dev = _get_device() if _get_device is not None else torch.cuda.current_device()
+    n = h * w
+    wp = (w + 63) >> 6
+    use_dev = n >= DEV_STAGE_MIN_PIXELS
+    st = getattr(_tls, "stage", None)
+    if st is None or st.device != dev or st.in_n < n or st.out_n < h * wp * 8 + 128 or \
+            (use_dev and st.dev_n < n):
+        st = _staging(n, h * wp * 8 + 128, dev, n if use_dev else 0)
     words = np.empty((h, wp), dtype=np.uint64)
-    dev = torch.cuda.current_device() if device_index is None else device_index
-    rc = _capi.fn("be_host_detect_u64_staged")(
-        pix.ctypes.data, pix.strides[0], h, w, fill_bit(border), 1 if edgeset else 0,
-        stage_in.data_ptr(), stage_in.numel(), stage_out.data_ptr(), stage_out.numel(),
-        words.ctypes.data, _raw_stream(dev) if _raw_stream is not None
-        else torch.cuda.current_stream(dev).cuda_stream)
+    if _staged_fn is None:
+        _staged_fn = _capi.fn("be_host_detect_u64_staged")
+    rc = _staged_fn(pix.ctypes.data, pix.strides[0], h, w, fb, 1 if edgeset else 0,
+                    st.in_ptr, st.in_n, st.out_ptr, st.out_n, st.dev_ptr if use_dev else None,
+                    words.ctypes.data,
+                    _raw_stream(dev) if _raw_stream is not None
+                    else torch.cuda.current_stream(dev).cuda_stream)
     if rc:
         _capi.check(rc)
-    words.setflags(write=False)
+    words.flags.writeable = False
     return words
 
 

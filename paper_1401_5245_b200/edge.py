@@ -24,15 +24,23 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from .bitimage import BitImage, BorderPolicy, Direction, PixelColor
 
 _WHITE = BorderPolicy.WHITE_OUTSIDE
 
 
-def _cuda():
-    from . import cuda
+_CU = None
 
-    return cuda
+
+def _cuda():
+    global _CU
+    if _CU is None:
+        from . import cuda
+
+        _CU = cuda
+    return _CU
 
 
 def build_mask(img: BitImage) -> BitImage:
@@ -56,7 +64,7 @@ def fundamental_edge(img: BitImage, mask: BitImage, side: Direction,
 
 def _edges(img: BitImage, border: BorderPolicy, edgeset: bool) -> BitImage:
     pix = img._take_pixels()
-    if pix is not None and not hasattr(pix, "t"):
+    if type(pix) is np.ndarray:
         # small host image, nothing uploaded yet: pack + edges in one kernel over
         # the thread's page-locked staging pair, words back, in one native call;
         # the result holds host words (uploaded on demand), the input keeps its

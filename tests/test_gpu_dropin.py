@@ -195,7 +195,7 @@ def test_host_flow_one_call(policy, cuda_dev):
         src = a.copy()
         img = BitImage.from_array(src)
         src[...] = 0                                        # the image owns its pixels
-        assert img._pix is not None and not img._pix.is_cuda
+        assert img._pix is not None and not getattr(img._pix, "is_cuda", False)
         e = detect_edges_mask(img, b)
         assert e._words is not None                         # downloaded by the same call
         assert (e.words == exp).all()
@@ -257,7 +257,8 @@ def test_large_host_array_packed_at_once(cuda_dev, monkeypatch):
     from paper_1401_5245_b200.edge import detect_edges_mask
 
     monkeypatch.setattr(B, "_PINNED_MAX", 1000)
-    for a in (_img(7, 40, 130), _img(8, 40, 130).astype(np.int32)):
+    # wider than the small-image flow's 1023 px: the page-locked path's limit applies
+    for a in (_img(7, 40, 1030), _img(8, 40, 1030).astype(np.int32)):
         img = B.BitImage.from_array(a)
         assert img._pix is None and img._dev is not None
         ref = P.from_array(a)
