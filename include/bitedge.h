@@ -255,6 +255,9 @@ int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_
 /* ---- misc ----------------------------------------------------------------- */
 const char *be_last_error(void);
 int be_abi_version(void);
+/* Re-read the BITEDGE_* dispatch knobs from the environment (they are read once,
+ * on the first call). */
+int be_reload_knobs(void);
 /* Number of kernels this thread has launched through the ABI (for bench.py's
  * gpu_launches accounting). */
 int64_t be_launch_count(void);

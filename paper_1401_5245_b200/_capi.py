@@ -61,6 +61,7 @@ _SIGNATURES = {
     "be_host_detect_u64": [_P, _I64, _I64, _INT, _INT, _P, _P, _P, _P, _P],
     "be_host_detect_u64_staged": [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _P, _P,
                                   _P],
+    "be_reload_knobs": [],
     "be_last_error": [],
     "be_abi_version": [],
     "be_launch_count": [],
@@ -119,6 +120,11 @@ def fn(name: str):
     """The typed foreign function itself (hot callers check the rc only when
     it is nonzero)."""
     return getattr(_lib if _lib is not None else load(), name)
+
+
+def reload_knobs() -> None:
+    """Re-read the BITEDGE_* dispatch knobs (read once per process otherwise)."""
+    check(load().be_reload_knobs())
 
 
 def launch_count() -> int:

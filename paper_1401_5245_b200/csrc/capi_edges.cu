@@ -34,7 +34,7 @@ int launch_tile(TileParams &tp, int64_t rows, cudaStream_t st) {
 // Kernel selection knob for A/B measurements: BITEDGE_KERNEL=tile forces the
 // one-shot tile kernel, =stream forbids nothing (default: stream when eligible).
 bool stream_allowed() {
-    const char *e = getenv("BITEDGE_KERNEL");
+    const char *e = knob(KN_KERNEL);
     return !(e && strcmp(e, "tile") == 0);
 }
 
@@ -68,7 +68,7 @@ int launch_stream_kind(StreamParams &sp, size_t smem, cudaStream_t st) {
 // kOutAll multi-output), 8-word items, whole items with no padding bits
 // (BITEDGE_K1_GENERIC turns them off).
 inline bool k1_aligned(bool single, int cw, int64_t w) {
-    return single && cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
+    return single && cw == 8 && w % 256 == 0 && !knob(KN_K1_GENERIC);
 }
 
 // Launch helpers: dispatch the runtime choices onto template parameters.
@@ -129,18 +129,18 @@ int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
             return kNoKernel;
         } else {
             // widest alignment every row start has (rp.v8 carries it: 8, 4 or 1)
-            if (rp.v8 == 8) launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, u8_block(), 0, st, rp);
-            else if (rp.v8 == 4) launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, u8_block(), 0, st, rp);
-            else launch_kb(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, u8_block(), 0, st, rp);
+            if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, 0, st, rp);
+            else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, 0, st, rp);
+            else launch_k(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, 0, st, rp);
             return cuda_check("edge_reg_u8_kernel<UNAL>");
         }
     }
     if (rp.v8) {
-        if (rs == 8) launch_kb(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, u8_block(), 0, st, rp);
-        else launch_kb(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, u8_block(), 0, st, rp);
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, true>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, true>, grid, 0, st, rp);
     } else {
-        if (rs == 8) launch_kb(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, u8_block(), 0, st, rp);
-        else launch_kb(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, u8_block(), 0, st, rp);
+        if (rs == 8) launch_k(edge_reg_u8_kernel<8, OUT, HALO, false>, grid, 0, st, rp);
+        else launch_k(edge_reg_u8_kernel<4, OUT, HALO, false>, grid, 0, st, rp);
     }
     return cuda_check("edge_reg_u8_kernel");
 }
@@ -221,8 +221,8 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     rp.thr = thr;
     {   // alignment of every row start (base and row stride)
         const uintptr_t a = (uintptr_t)in | (uintptr_t)in_row_bytes;
-        rp.v8 = (a % 8 == 0 && !getenv("BITEDGE_UNAL_BYTES")) ? 8
-              : (a % 4 == 0 && !getenv("BITEDGE_UNAL_BYTES")) ? 4 : 1;
+        rp.v8 = (a % 8 == 0 && !knob(KN_UNAL_BYTES)) ? 8
+              : (a % 4 == 0 && !knob(KN_UNAL_BYTES)) ? 4 : 1;
     }
     constexpr int rs = 4;
     rp.nstrips = (row_hi - row_lo + rs - 1) / rs;
@@ -237,20 +237,20 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
             uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
             int64_t row_lo, int64_t row_hi, cudaStream_t st, int thr) {
-    const char *e = getenv("BITEDGE_KERNEL");
+    const char *e = knob(KN_KERNEL);
     if (e && (strcmp(e, "tile") == 0 || strcmp(e, "stream") == 0)) return kNoKernel;
     auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
     // packed rows that are only 4-byte aligned (not 16-byte multiples, or a
     // strided view): K1's UNAL items, without halos
     const bool unal = input_kind == 0 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
                       !below && ((uintptr_t)in % 4) == 0 && in_row_bytes % 4 == 0 &&
-                      !getenv("BITEDGE_NO_UNAL");
+                      !knob(KN_NO_UNAL);
     // uint8 rows at any byte (row lengths that are not 16-byte multiples): K2's
     // UNAL strips, single-output, without halos
     const bool sides0 = o_side[0] || o_side[1] || o_side[2] || o_side[3];
     const bool u8unal = input_kind == 1 && (!al16(in) || in_row_bytes % 16 != 0) && !above &&
                         !below && !sides0 && (o_edges || o_eset || o_packed) &&
-                        !getenv("BITEDGE_NO_UNAL");
+                        !knob(KN_NO_UNAL);
     if (u8unal) return try_reg_u8_unal(in, in_row_bytes, o_edges, o_eset, o_packed, out_stride_u32, G, nrows,
                                        row_lo, row_hi, st, thr);
     if (!unal && (!al16(in) || !al16(above) || !al16(below) || in_row_bytes % 16 != 0))
@@ -268,7 +268,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // >= 1024 px wide) and K2 store the swapped halves (oswap); K2w / K2r / K2t do
     // not, and the four side outputs go to the tile kernel
     const bool u64_out = input_kind == 1 && G.swap;
-    const bool u64_k2 = u64_out && (G.w < 1024 || getenv("BITEDGE_NO_TMA"));
+    const bool u64_k2 = u64_out && (G.w < 1024 || knob(KN_NO_TMA));
     // K2 writes edges / EdgeSet plus, optionally, the packed words; nothing else
     const bool k2_outs = !sides0 && (o_edges || o_eset || o_packed);
     if (u64_k2 && !k2_outs) return kNoKernel;
@@ -284,16 +284,16 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // 5.3 / 79 % for 4-word x 4-row items; scripts/c3sweep.sh).
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
     const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
-    int cw = (input_kind == 0 && in32 && !multi && !getenv("BITEDGE_CW4")) ? 8 : 4;
+    int cw = (input_kind == 0 && in32 && !multi && !knob(KN_CW4)) ? 8 : 4;
     if (unal) {
         if (multi) return kNoKernel;
         rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + (int64_t)G.wp * 4;
-        rp.unal_words = getenv("BITEDGE_UNAL_CHUNKS") == nullptr;   // words: measured faster
+        rp.unal_words = knob(KN_UNAL_CHUNKS) == nullptr;   // words: measured faster
     }
     // (uint64 words take 2-row strips only in the tail-free and UNAL kernels)
     const bool swap2 = !G.swap || unal || k1_aligned(!multi, cw, G.w);
     const int packed_rs = (input_kind == 0 && swap2 && !big) ? 2 : 4;
-    if (input_kind == 0 && in32 && !multi && getenv("BITEDGE_CW8")) cw = 8;
+    if (input_kind == 0 && in32 && !multi && knob(KN_CW8)) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
     rp.thr = thr;
@@ -303,7 +303,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     rp.vst = rp.vst && al(o_packed, 4 * ocw);
     if (input_kind == 1 && !multi && !u64_out && !above && !below && row_lo == 0 && row_hi == nrows &&
         in_row_bytes == G.w && ((uintptr_t)in % 32) == 0 && G.w % 32 == 0 && G.wp <= 32 &&
-        (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !getenv("BITEDGE_NO_WARPIMG")) {
+        (G.wp & (G.wp - 1)) == 0 && out_stride_u32 == G.wp && !knob(KN_NO_WARPIMG)) {
         const int lwpr = ilog2(G.wp), rpi = 32 >> lwpr;
         if (G.h % rpi == 0 && G.h / rpi <= 8) {
             const int groups = (int)(G.h / rpi);
@@ -329,14 +329,14 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
                 // GMAX = 4 (48 regs, one wave of 4096 C2 images) is 1.5 % faster with
                 // overlapped batches but 9 % slower serially under PDL than GMAX = 8
                 // (77 regs, 1.15 waves): opt-in knob.
-                const bool g8 = getenv("BITEDGE_WARPIMG_G4") == nullptr;
+                const bool g8 = knob(KN_WARPIMG_G4) == nullptr;
                 // (Capping residency at one wave with 128-thread CTAs + 32 KB of
                 // dummy smem -- 28 warps/SM, 4144 slots for 4096 images -- was
                 // 20 % slower overlapped and serially: not taken.)
                 const unsigned wblock = (unsigned)kThreads;
                 const unsigned wgrid = (unsigned)grid;
                 const size_t wsmem = 0;
-                rp.pdl_late = getenv("BITEDGE_PDL_LATE") != nullptr;
+                rp.pdl_late = knob(KN_PDL_LATE) != nullptr;
                 switch (lwpr) {
                     BE_WARPIMG(0)
                     BE_WARPIMG(1)
@@ -353,31 +353,31 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
-    if (input_kind == 1 && (G.w >= 2048 || (u64_out && !u64_k2)) && !getenv("BITEDGE_NO_TMA") &&
-        (!getenv("BITEDGE_TMA1") || u64_out)) {
+    if (input_kind == 1 && (G.w >= 2048 || (u64_out && !u64_k2)) && !knob(KN_NO_TMA) &&
+        (!knob(KN_TMA1) || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
-        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr || (u64_out && getenv("BITEDGE_U64_TMA"));
+        const bool force = knob(KN_FORCE_TMA) != nullptr || (u64_out && knob(KN_U64_TMA));
         if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
             // strips, so the last wave's tail is a quarter as long: C5 737 ->
             // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
             // where the 25 % extra staged halo rows of 8-row strips cost more
             // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
-            const bool short_strips = (thr == 1 || getenv("BITEDGE_TMA2_RSL8")) &&
-                                      !getenv("BITEDGE_TMA2_RSL32");
+            const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) &&
+                                      !knob(KN_TMA2_RSL32);
             const bool halo = above || below;
             return short_strips ? launch_tma2<8>(rp, multi, halo, nseg, st)
                                 : launch_tma2<32>(rp, multi, halo, nseg, st);
         }
     }
     if (!k2_outs && input_kind == 1) return kNoKernel;   // other uint8 multi-output: tile kernel
-    if (input_kind == 1 && !u64_out && !o_packed && G.w >= 1024 && !getenv("BITEDGE_NO_TMA")) {
+    if (input_kind == 1 && !u64_out && !o_packed && G.w >= 1024 && !knob(KN_NO_TMA)) {
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
         const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
         const int64_t nwarps = nstrips * nseg;
-        const bool force = getenv("BITEDGE_FORCE_TMA") != nullptr;   // tests: any size
+        const bool force = knob(KN_FORCE_TMA) != nullptr;   // tests: any size
         if ((force || nwarps >= (int64_t)sm_count() * 32) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
             const unsigned grid = (unsigned)((nwarps + 7) / 8);
             const size_t smem = (size_t)8 * kD * 1056 + (size_t)8 * kD * 8;
@@ -403,7 +403,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
     constexpr int kRSL = 32, kQ = 4;
-    if (input_kind == 1 && rp.v8 && !u64_out && !o_packed && !getenv("BITEDGE_NO_ROLL") &&
+    if (input_kind == 1 && rp.v8 && !u64_out && !o_packed && !knob(KN_NO_ROLL) &&
         (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
         rp.nstrips = (rows + kRSL - 1) / kRSL;
         const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
@@ -426,19 +426,17 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // strip height: 4 rows (the one-shot kernels keep every row of the strip in flight)
     int rs = input_kind == 0 ? packed_rs : 4;
     if (input_kind == 1) {
-        const char *rse = getenv("BITEDGE_RS");
+        const char *rse = knob(KN_RS);
         if (rse) rs = atoi(rse) == 8 ? 8 : 4;
     } else if (!G.swap) {
-        const char *rse = getenv("BITEDGE_PRS");      // packed strip height experiments: 2/4/8
+        const char *rse = knob(KN_PRS);      // packed strip height experiments: 2/4/8
         if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
     }
     if ((multi || rp.in_end) && rs == 8) rs = 4;     // kOutAll / UNAL: 2- and 4-row strips
-    if (rp.in_end && getenv("BITEDGE_UNAL_RS4")) rs = 4;
+    if (rp.in_end && knob(KN_UNAL_RS4)) rs = 4;
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;
-    // K2 on zero-copy host input takes the caller's (smaller) block size
-    const int64_t blk = (input_kind == 1 && !multi_out(rp)) ? u8_block() : kThreads;
-    const int64_t grid = (threads + blk - 1) / blk;
+    const int64_t grid = (threads + kThreads - 1) / kThreads;
     if (grid > 0x7FFFFFFFLL) return kNoKernel;
     if (above || below)
         return launch_reg_halo<true>(rp, input_kind, G.swap, cw, rs, (unsigned)grid, st);

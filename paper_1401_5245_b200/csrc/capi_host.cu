@@ -1,9 +1,13 @@
 // capi_host.cu -- host-buffer pipelines (the end-to-end path), CUDA IPC for
 // peer-memory halos, and the ABI's bookkeeping entry points.  Owns the library's
-// only state: a thread-local error string and launch counter.
+// only state: a thread-local error string and launch counter, and the cached
+// copy of the BITEDGE_* dispatch knobs (read once; be_reload_knobs).
 #include "capi_internal.cuh"
 
 #include <time.h>
+
+#include <atomic>
+#include <mutex>
 
 using namespace bitedge;
 using namespace bitedge::capi;
@@ -12,11 +16,53 @@ namespace bitedge {
 namespace capi {
 thread_local char g_err[512];
 thread_local int64_t g_launches = 0;
-thread_local int g_u8_block = 0;
+
+const char *const kKnobNames[KN_COUNT] = {
+    "BITEDGE_KERNEL", "BITEDGE_K1_GENERIC", "BITEDGE_UNAL_BYTES", "BITEDGE_NO_UNAL",
+    "BITEDGE_NO_TMA", "BITEDGE_CW4", "BITEDGE_UNAL_CHUNKS", "BITEDGE_CW8",
+    "BITEDGE_NO_WARPIMG", "BITEDGE_WARPIMG_G4", "BITEDGE_PDL_LATE", "BITEDGE_TMA1",
+    "BITEDGE_FORCE_TMA", "BITEDGE_U64_TMA", "BITEDGE_TMA2_RSL8", "BITEDGE_TMA2_RSL32",
+    "BITEDGE_NO_ROLL", "BITEDGE_RS", "BITEDGE_PRS", "BITEDGE_UNAL_RS4", "BITEDGE_P4_UNFUSED",
+    "BITEDGE_P4_BYTES", "BITEDGE_PDL"};
+}  // namespace capi
+}  // namespace bitedge
+
+namespace {
+// copies of the knob values (the environment's own strings may be freed when it changes)
+char g_knob_val[bitedge::capi::KN_COUNT][64];
+bool g_knob_set[bitedge::capi::KN_COUNT];
+std::atomic<int> g_knobs_loaded{0};
+std::mutex g_knob_mu;
+
+void load_knobs_locked() {
+    for (int k = 0; k < bitedge::capi::KN_COUNT; ++k) {
+        const char *v = getenv(bitedge::capi::kKnobNames[k]);
+        g_knob_set[k] = v != nullptr;
+        if (v) snprintf(g_knob_val[k], sizeof(g_knob_val[k]), "%s", v);
+    }
+    g_knobs_loaded.store(1, std::memory_order_release);
+}
+}  // namespace
+
+namespace bitedge {
+namespace capi {
+const char *knob(Knob k) {
+    if (!g_knobs_loaded.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lk(g_knob_mu);
+        if (!g_knobs_loaded.load(std::memory_order_relaxed)) load_knobs_locked();
+    }
+    return g_knob_set[k] ? g_knob_val[k] : nullptr;
+}
 }  // namespace capi
 }  // namespace bitedge
 
 extern "C" {
+
+int be_reload_knobs(void) {
+    std::lock_guard<std::mutex> lk(g_knob_mu);
+    load_knobs_locked();
+    return BE_OK;
+}
 
 const char *be_last_error(void) { return g_err; }
 int be_abi_version(void) { return BE_ABI_VERSION; }
@@ -240,42 +286,13 @@ int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_
     // one launch reading the pixels (mapped page-locked staging over PCIe, or
     // HBM) and writing the words into the mapped page-locked staging buffer:
     // pack (bitimage.py:122-136) + edges, uint64 words
-    static const int zc_block = [] {
-        const char *e = getenv("BITEDGE_ZC_BLOCK");       // experiments: 32..256
-        return e ? atoi(e) : 0;
-    }();
-    if (!dev_stage_or_null) g_u8_block = zc_block;
     rc = edges_impl(src, 1, w, nullptr, nullptr, emit_edgeset ? nullptr : dst,
                     emit_edgeset ? dst : nullptr, side, nullptr, 64, wp, 1, h, w, fill_bit, 0, h,
                     st);
-    g_u8_block = 0;
     if (rc) return rc;
     if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[2]);
-    // completion: BITEDGE_STAGED_SPIN=1 (experiments) enqueues a stream write of a
-    // per-thread sequence number into page-locked memory after the kernel and
-    // spins on it; otherwise cudaStreamSynchronize
-    static const bool spin = getenv("BITEDGE_STAGED_SPIN") != nullptr;
-    static thread_local uint32_t seq = 0;
-    uint32_t *flag = (uint32_t *)((char *)stage_out + ((stage_out_bytes - 64) & ~(int64_t)63));
-    cudaError_t e = cudaSuccess;
-    if (spin && stage_out_bytes - 64 >= h * wp * 8) {
-        ++seq;
-        rc = be_stream_write32(flag, seq, stream);
-        if (rc) return rc;
-        for (uint64_t i = 1;; ++i) {
-            if (*(volatile uint32_t *)flag == seq) break;
-            if ((i & 4095) == 0 && (e = cudaStreamQuery(st)) != cudaErrorNotReady) {
-                if (e != cudaSuccess) break;
-                if (*(volatile uint32_t *)flag == seq) break;
-            }
-        }
-        if (e != cudaSuccess && e != cudaErrorNotReady)
-            return fail((int)e, "sync: %s", cudaGetErrorString(e));
-    } else {
-        e = cudaStreamSynchronize(st);
-    }
-    if (e != cudaSuccess && e != cudaErrorNotReady)
-        return fail((int)e, "sync: %s", cudaGetErrorString(e));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
     if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[3]);
     memcpy(words_out, stage_out, (size_t)(h * wp * 8));
     if (trace) {

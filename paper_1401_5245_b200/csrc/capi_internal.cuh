@@ -17,15 +17,43 @@
 namespace bitedge {
 namespace capi {
 
-// the only state: this thread's error text and launch counter (capi_host.cu),
-// and the block size K2 uses for the call in progress (set by the zero-copy
-// host flows, whose kernels read pinned host memory: smaller CTAs spread the
-// PCIe reads over more SMs; 0 = kThreads)
+// the only state: this thread's error text and launch counter (capi_host.cu)
 extern thread_local char g_err[512];
 extern thread_local int64_t g_launches;
-extern thread_local int g_u8_block;
 
-inline unsigned u8_block() { return g_u8_block > 0 ? (unsigned)g_u8_block : (unsigned)kThreads; }
+// Dispatch knobs: BITEDGE_<name> environment variables
+// for A/B measurements and the variant tests, read once per process on first
+// use (be_reload_knobs re-reads them) -- a getenv per knob per call cost ~1.4 us
+// of host time per launch with a typical environment.
+enum Knob : int {
+    KN_KERNEL,
+    KN_K1_GENERIC,
+    KN_UNAL_BYTES,
+    KN_NO_UNAL,
+    KN_NO_TMA,
+    KN_CW4,
+    KN_UNAL_CHUNKS,
+    KN_CW8,
+    KN_NO_WARPIMG,
+    KN_WARPIMG_G4,
+    KN_PDL_LATE,
+    KN_TMA1,
+    KN_FORCE_TMA,
+    KN_U64_TMA,
+    KN_TMA2_RSL8,
+    KN_TMA2_RSL32,
+    KN_NO_ROLL,
+    KN_RS,
+    KN_PRS,
+    KN_UNAL_RS4,
+    KN_P4_UNFUSED,
+    KN_P4_BYTES,
+    KN_PDL,
+    KN_COUNT
+};
+extern const char *const kKnobNames[KN_COUNT];
+// the knob's value, or nullptr when unset
+const char *knob(Knob k);
 
 inline int fail(int code, const char *fmt, ...) {
     va_list ap;
@@ -103,7 +131,7 @@ inline int check_ptr(const void *p, int word_bits, const char *what) {
 // kernel's CTAs may be scheduled while the previous kernel on the stream drains;
 // they block in griddepcontrol.wait until its results are visible.
 inline bool pdl_enabled() {
-    const char *e = getenv("BITEDGE_PDL");
+    const char *e = knob(KN_PDL);
     return !(e && e[0] == '0');
 }
 

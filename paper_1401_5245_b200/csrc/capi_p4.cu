@@ -192,7 +192,7 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
     cudaStream_t st = S(stream);
     auto al = [](const void *p, int a) { return ((uintptr_t)p % a) == 0; };
     // fused path: P4 rows are whole 16-byte chunks -> K1 reads and writes P4 directly
-    if (rb % 16 == 0 && al(p4_in, 16) && al(p4_out, 16) && !getenv("BITEDGE_P4_UNFUSED") &&
+    if (rb % 16 == 0 && al(p4_in, 16) && al(p4_out, 16) && !knob(KN_P4_UNFUSED) &&
         n * h < ((int64_t)1 << 31)) {
         RegParams rp;
         memset(&rp, 0, sizeof(rp));
@@ -213,7 +213,7 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
         const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
         K1Div dv;
         if (grid <= 0x7FFFFFFFLL && k1_setup(rp, dv)) {
-            const bool aligned = cw == 8 && w % 256 == 0 && !getenv("BITEDGE_K1_GENERIC");
+            const bool aligned = cw == 8 && w % 256 == 0 && !knob(KN_K1_GENERIC);
             if (aligned && rs == 4)
                 launch_k(edge_reg_packed_kernel<0, 4, 8, kOutEdges, false, true, true>, (unsigned)grid,
                          0, st, rp, dv);
@@ -237,13 +237,13 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
     }
     // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items cut
     // out of aligned 16-byte chunks (UNAL)
-    if (rb % 4 == 0 && al(p4_in, 4) && al(p4_out, 4) && !getenv("BITEDGE_P4_UNFUSED") &&
-        !getenv("BITEDGE_P4_BYTES") && n * h < ((int64_t)1 << 31)) {
+    if (rb % 4 == 0 && al(p4_in, 4) && al(p4_out, 4) && !knob(KN_P4_UNFUSED) &&
+        !knob(KN_P4_BYTES) && n * h < ((int64_t)1 << 31)) {
         RegParams rp;
         memset(&rp, 0, sizeof(rp));
         rp.in = (const char *)p4_in; rp.in_row_bytes = rb;
         rp.in_end = (const char *)p4_in + n * h * rb;
-        rp.unal_words = getenv("BITEDGE_UNAL_CHUNKS") == nullptr;   // words: measured faster
+        rp.unal_words = knob(KN_UNAL_CHUNKS) == nullptr;   // words: measured faster
         rp.o_edges = (uint32_t *)p4_out; rp.out_stride = rb / 4;
         rp.nrows = n * h; rp.row_lo = 0; rp.row_hi = n * h;
         rp.h = (uint32_t)h; rp.w = w; rp.wp = G.wp; rp.pl = G.pl;
@@ -270,7 +270,7 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
     constexpr int kR = 8;
     const int64_t nstrips = (n * h + kR - 1) / kR;
     const bool fits = nstrips * G.wp + 256 < ((int64_t)1 << 32) && n * h < ((int64_t)1 << 32) - kR;
-    if (!getenv("BITEDGE_P4_UNFUSED") && fits) {
+    if (!knob(KN_P4_UNFUSED) && fits) {
         WordGeom g = word_geom(G, G.wp);
         const int64_t threads = nstrips * g.wp;
         p4_edges_bytes_kernel<kR><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(

@@ -485,8 +485,7 @@ edge_reg_u8_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
     const Thr T = make_thr(p.thr);
-    // blockDim: kThreads, or fewer for zero-copy host input (more SMs issuing PCIe reads)
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t strip = t / p.items;
     const int c = (int)(t - strip * p.items);          // output word of the row

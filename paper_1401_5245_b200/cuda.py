@@ -264,36 +264,28 @@ def host_detect(host_pixels: torch.Tensor, border=WHITE_OUTSIDE, *, edgeset: boo
 # staging pair (plus one device staging buffer) per calling thread, reused by
 # every call -- a fixed footprint however many images are in flight in Python
 SMALL_MAX_PIXELS = 1 << 20
-# from this many pixels on, the pixels cross PCIe by one copy-engine transfer
-# instead of being read by the kernel from mapped memory (scripts/dropin_breakdown.py)
-DEV_STAGE_MIN_PIXELS = int(os.environ.get("BITEDGE_DEV_STAGE_MIN", 1 << 40))
 _tls = threading.local()
 _staged_fn = None
 _get_device = getattr(torch._C, "_cuda_getDevice", None)
 
 
 class _Stage:
-    __slots__ = ("pin_in", "pin_out", "dev", "in_ptr", "in_n", "out_ptr", "out_n", "dev_ptr",
-                 "dev_n", "device")
+    __slots__ = ("pin_in", "pin_out", "in_ptr", "in_n", "out_ptr", "out_n", "device")
 
-    def __init__(self, in_bytes, out_bytes, dev_bytes, device):
+    def __init__(self, in_bytes, out_bytes, device):
         self.pin_in = torch.empty(in_bytes, dtype=torch.uint8, pin_memory=True)
         self.pin_out = torch.empty(out_bytes, dtype=torch.uint8, pin_memory=True)
-        self.dev = torch.empty(max(1, dev_bytes), dtype=torch.uint8,
-                               device=torch.device("cuda", device))
         self.in_ptr, self.in_n = self.pin_in.data_ptr(), in_bytes
         self.out_ptr, self.out_n = self.pin_out.data_ptr(), out_bytes
-        self.dev_ptr, self.dev_n = self.dev.data_ptr(), dev_bytes
         self.device = device
 
 
-def _staging(in_bytes: int, out_bytes: int, device: int, dev_bytes: int = 0) -> _Stage:
+def _staging(in_bytes: int, out_bytes: int, device: int) -> _Stage:
+    """This thread's page-locked staging pair for the ctypes path (grown on demand)."""
     st = getattr(_tls, "stage", None)
-    if st is None or st.device != device or st.in_n < in_bytes or st.out_n < out_bytes or \
-            st.dev_n < dev_bytes:
-        keep = (0, 0, 0) if st is None or st.device != device else (st.in_n, st.out_n, st.dev_n)
-        st = _Stage(max(in_bytes, keep[0], 64 << 10), max(out_bytes, keep[1], 16 << 10),
-                    max(dev_bytes, keep[2]), device)
+    if st is None or st.device != device or st.in_n < in_bytes or st.out_n < out_bytes:
+        keep = (0, 0) if st is None or st.device != device else (st.in_n, st.out_n)
+        st = _Stage(max(in_bytes, keep[0], 64 << 10), max(out_bytes, keep[1], 16 << 10), device)
         _tls.stage = st
     return st
 
@@ -324,8 +316,8 @@ def host_detect_small(pix: np.ndarray, border=WHITE_OUTSIDE, *, edgeset: bool = 
     host memory (nonzero = white; W < 1024, H*W <= SMALL_MAX_PIXELS) -> a fresh
     read-only uint64 words array [H, ceil(W/64)].  The pixels go through this
     thread's page-locked staging pair; one kernel packs and detects, reading the
-    pixels over PCIe (or from HBM after one copy-engine transfer, for images of
-    DEV_STAGE_MIN_PIXELS and more) and writing the words into the staging pair."""
+    pixels and writing the words over PCIe (a copy-engine transfer of the pixels
+    was slower at every size up to 1 Mpx, scripts/dropin_breakdown.py)."""
     global _staged_fn
     if _dropin is not None:
         fb = getattr(border, "value", border)
@@ -352,16 +344,14 @@ def host_detect_small(pix: np.ndarray, border=WHITE_OUTSIDE, *, edgeset: bool = 
     dev = _get_device() if _get_device is not None else torch.cuda.current_device()
     n = h * w
     wp = (w + 63) >> 6
-    use_dev = n >= DEV_STAGE_MIN_PIXELS
     st = getattr(_tls, "stage", None)
-    if st is None or st.device != dev or st.in_n < n or st.out_n < h * wp * 8 + 128 or \
-            (use_dev and st.dev_n < n):
-        st = _staging(n, h * wp * 8 + 128, dev, n if use_dev else 0)
+    if st is None or st.device != dev or st.in_n < n or st.out_n < h * wp * 8 + 128:
+        st = _staging(n, h * wp * 8 + 128, dev)
     words = np.empty((h, wp), dtype=np.uint64)
     if _staged_fn is None:
         _staged_fn = _capi.fn("be_host_detect_u64_staged")
     rc = _staged_fn(pix.ctypes.data, pix.strides[0], h, w, fb, 1 if edgeset else 0,
-                    st.in_ptr, st.in_n, st.out_ptr, st.out_n, st.dev_ptr if use_dev else None,
+                    st.in_ptr, st.in_n, st.out_ptr, st.out_n, None,
                     words.ctypes.data,
                     _raw_stream(dev) if _raw_stream is not None
                     else torch.cuda.current_stream(dev).cuda_stream)

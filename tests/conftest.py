@@ -50,6 +50,36 @@ def encode_bits(arr: np.ndarray) -> np.ndarray:
     return (flat * weights).sum(1).astype(np.uint16)
 
 
+@pytest.fixture(autouse=True)
+def _dispatch_knobs(monkeypatch):
+    """The library reads its BITEDGE_* dispatch knobs once per process: re-read
+    them at the start of every test and after every monkeypatch.setenv/delenv
+    (the knob-sweeping tests set them inside the test body)."""
+    import importlib
+
+    def reload():
+        try:
+            capi = importlib.import_module("paper_1401_5245_b200._capi")
+            if capi._lib is not None:
+                capi.reload_knobs()
+        except Exception:
+            pass
+
+    setenv, delenv = monkeypatch.setenv, monkeypatch.delenv
+
+    def setenv_(name, value, prepend=None):
+        setenv(name, value, prepend)
+        reload()
+
+    def delenv_(name, raising=True):
+        delenv(name, raising)
+        reload()
+
+    monkeypatch.setenv, monkeypatch.delenv = setenv_, delenv_
+    reload()
+    yield
+
+
 @pytest.fixture(scope="session")
 def cuda_dev():
     import torch

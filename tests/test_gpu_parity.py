@@ -620,14 +620,18 @@ def test_pbm_roundtrip_and_detect(cuda_dev):
 
         # default dispatch (K1 on 16-byte or 4-byte rows, else the byte kernel),
         # the byte kernel forced, and decode -> K1 -> encode
+        from paper_1401_5245_b200 import _capi
+
         for knob in (None, "BITEDGE_P4_BYTES", "BITEDGE_P4_UNFUSED"):
             if knob:
                 os.environ[knob] = "1"
+                _capi.reload_knobs()
             try:
                 got = read_pbm(detect_pbm(p4)).to_array()
             finally:
                 if knob:
                     os.environ.pop(knob, None)
+                    _capi.reload_knobs()
             assert (got == exp).all(), (h, w, knob)
         # P4 padding bits of the output are zero
         if w % 8:
