@@ -14,7 +14,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libbitedge_cuda.so")
 # one translation unit per concern, compiled in parallel then linked
 SOURCES = ["capi_edges.cu", "capi_words.cu", "capi_p4.cu", "capi_host.cu"]
-HEADERS = ["capi_internal.cuh", "edge_tile.cuh", "edge_stream.cuh", "edge_reg.cuh",
+HEADERS = ["capi_internal.cuh", "edge_tile.cuh", "edge_stream.cuh", "edge_reg.cuh", "edge_flat.cuh",
            os.path.join("..", "..", "include", "bitedge.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -2,6 +2,7 @@
 // TMA-stream / register-direct K1, K2, K2w, K2r, K2t, K2t2, halos, multi-output)
 // and the C-ABI entry points that compute edges (include/bitedge.h).
 #include "capi_internal.cuh"
+#include "edge_flat.cuh"
 #include "edge_reg.cuh"
 #include "edge_stream.cuh"
 
@@ -233,6 +234,58 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     return launch_reg_u8<kOutEdges, false>(rp, rs, (unsigned)grid, st);
 }
 
+// K1f (edge_flat.cuh): packed rows with row stride == words per row that is not a
+// multiple of the vector width, edges and / or EdgeSet, no halos.
+template <int CW, int SWAP, int OUT>
+int launch_flat_cw(const FlatParams &fp, int ru, unsigned grid, cudaStream_t st) {
+#define BE_FLAT(R)                                                                    \
+    if constexpr (R < CW && (!SWAP || R % 2 == 0))                                    \
+        if (ru == R) {                                                                \
+            launch_k(edge_flat_kernel<CW, SWAP, (R < CW ? R : 1), OUT>, grid, 0, st, fp); \
+            return cuda_check("edge_flat_kernel");                                    \
+        }
+    BE_FLAT(1) BE_FLAT(2) BE_FLAT(3) BE_FLAT(4) BE_FLAT(5) BE_FLAT(6) BE_FLAT(7)
+#undef BE_FLAT
+    return kNoKernel;
+}
+
+int try_flat(const void *in, uint32_t *o_edges, uint32_t *o_eset, const Geometry &G,
+             int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
+    if (knob(KN_NO_FLAT)) return kNoKernel;
+    const int64_t S = G.wp;                                    // uint32 words per row
+    const int64_t nwords = nrows * S;
+    if (row_lo != 0 || row_hi != nrows || nwords >= ((int64_t)1 << 31) - 64 || S < 16 ||
+        G.h >= ((int64_t)1 << 31))
+        return kNoKernel;
+    auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+    const int cw = (al(in, 32) && al(o_edges, 32) && al(o_eset, 32)) ? 8
+                 : (al(in, 16) && al(o_edges, 16) && al(o_eset, 16)) ? 4 : 0;
+    if (cw == 0 || S % cw == 0) return kNoKernel;
+    FlatParams fp;
+    memset(&fp, 0, sizeof(fp));
+    fp.in = (const uint32_t *)in;
+    fp.o_edges = o_edges; fp.o_eset = o_eset;
+    fp.nwords = (uint32_t)nwords; fp.S = (uint32_t)S; fp.h = (uint32_t)G.h;
+    fp.nrows = (uint32_t)nrows;
+    fp.pl = G.pl; fp.lastbit = G.lastbit; fp.padmask = G.padmask; fp.fillword = G.fillword;
+    fp.nchunks = (uint32_t)((nwords + cw - 1) / cw);
+    fp.div_s = make_fastdiv((uint32_t)S);
+    fp.div_h = make_fastdiv((uint32_t)G.h);
+    const int ru = (int)((cw - S % cw) % cw);
+    const unsigned grid = (fp.nchunks + kThreads - 1) / kThreads;
+    const int out = (o_edges && o_eset) ? kOutAny : o_eset ? kOutEset : kOutEdges;
+#define BE_FLAT_OUT(CWV, SW)                                                               \
+    return out == kOutAny ? launch_flat_cw<CWV, SW, kOutAny>(fp, ru, grid, st)             \
+         : out == kOutEset ? launch_flat_cw<CWV, SW, kOutEset>(fp, ru, grid, st)           \
+                           : launch_flat_cw<CWV, SW, kOutEdges>(fp, ru, grid, st);
+    if (cw == 8) {
+        if (G.swap) { BE_FLAT_OUT(8, 1) } else { BE_FLAT_OUT(8, 0) }
+    } else {
+        if (G.swap) { BE_FLAT_OUT(4, 1) } else { BE_FLAT_OUT(4, 0) }
+    }
+#undef BE_FLAT_OUT
+}
+
 int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *above,
             const void *below, uint32_t *o_edges, uint32_t *o_eset, uint32_t *const o_side[4],
             uint32_t *o_packed, int64_t out_stride_u32, const Geometry &G, int64_t nrows,
@@ -287,6 +340,12 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     int cw = (input_kind == 0 && in32 && !multi && !knob(KN_CW4)) ? 8 : 4;
     if (unal) {
         if (multi) return kNoKernel;
+        // contiguous rows (stride == row length): the flat kernel's aligned vector
+        // accesses instead of K1's word-by-word items
+        if (in_row_bytes == (int64_t)G.wp * 4 && out_stride_u32 == G.wp) {
+            const int rc = try_flat(in, o_edges, o_eset, G, nrows, row_lo, row_hi, st);
+            if (rc != kNoKernel) return rc;
+        }
         rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + (int64_t)G.wp * 4;
         rp.unal_words = knob(KN_UNAL_CHUNKS) == nullptr;   // words: measured faster
     }

@@ -49,6 +49,7 @@ enum Knob : int {
     KN_P4_UNFUSED,
     KN_P4_BYTES,
     KN_PDL,
+    KN_NO_FLAT,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

@@ -1,0 +1,202 @@
+// edge_flat.cuh -- K1f: the fused edge kernel for packed rows whose length is
+// NOT a multiple of the vector width (SURVEY 8(a) A7 on ragged widths: u32 rows
+// of w = 8000 px are 250 words; the drop-in's uint64 BitImage words,
+// bitimage.py:91-97, have an odd count whenever w % 128 is in 1..64).
+//
+// K1 walks column items of row strips, so on such rows every row starts at a
+// different 16-byte phase and its items are loaded word by word.  K1f instead
+// views the raster (contiguous rows: row stride == words per row == S) as ONE
+// flat word array and gives every thread one aligned chunk of CW words of it:
+//
+//   * centre:  one aligned CW-word vector load of the chunk itself;
+//   * up/down: the words at flat -S / +S are at a fixed phase RU = (-S) mod CW
+//     / RD = S mod CW from the chunk grid -- the same for every chunk of the
+//     launch -- so each lane loads the aligned chunk containing their start and
+//     takes the remaining RU (RD) words from the next lane by warp shuffle
+//     (consecutive lanes own consecutive chunks); RU is a template parameter,
+//     so the realignment is register moves;
+//   * left/right: the neighbouring lanes' edge words by shuffle (one scalar
+//     load for lanes 0 / 31);
+//   * row structure per word: column c = flat mod S and row = flat div S
+//     (multiply-shift division by launch constants); column 0 takes the left
+//     fill, the word holding pixel w-1 the right fill and the padding force,
+//     pure padding words (uint64 rows) are forced to 1, and the first / last
+//     row of every image take the vertical fill (bitimage.py:216-239);
+//   * one aligned vector store of the chunk (output stride == input stride).
+//
+// Every load and store is an aligned 16/32-byte access; DRAM traffic stays one
+// read of the input and one write of the output (up / centre / down rows of a
+// chunk are the same lines other warps read: L2 hits).  Chunks near the first
+// and last row (where a clamped vector load would not cover the words a
+// straddling chunk needs) and the ragged last chunk reload their words one by
+// one, bounded by the buffer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "edge_reg.cuh"
+
+namespace bitedge {
+
+struct FlatParams {
+    const uint32_t *in;      // CW*4-byte aligned
+    uint32_t *o_edges;       // CW*4-byte aligned (or nullptr)
+    uint32_t *o_eset;
+    uint32_t nwords;         // nrows * S  (< 2^31)
+    uint32_t S;              // row length == row stride, uint32 words (>= 2 * CW)
+    uint32_t h;              // rows per image
+    uint32_t nrows;
+    int pl;                  // last pixel word (pixel order) holding a visible pixel
+    uint32_t lastbit, padmask, fillword;
+    uint32_t nchunks;        // ceil(nwords / CW)
+    FastDiv div_s, div_h;
+};
+
+template <int CW>
+__device__ __forceinline__ void flat_load(const uint32_t *p, uint32_t (&v)[CW]) {
+    if constexpr (CW == 8) {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7])
+                     : "l"(p));
+    } else {
+        const uint4 q = ldg_stream_v4(p);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    }
+}
+
+// SWAP: uint64 words (pixel word p at uint32 index p ^ 1); chunks hold whole pairs.
+template <int CW, int SWAP, int RU, int OUT>
+__global__ void __launch_bounds__(kThreads)
+edge_flat_kernel(const FlatParams p) {
+    static_assert(RU > 0 && RU < CW && (!SWAP || RU % 2 == 0), "phase");
+    constexpr int RD = CW - RU;                       // S mod CW
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t t = blockIdx.x * kThreads + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool live = t < p.nchunks;
+    const uint32_t q = live ? t : p.nchunks - 1;      // dead lanes mirror the last chunk
+    const uint32_t base = q * CW;
+    const uint32_t S = p.S;
+    const uint32_t full = p.nwords / CW;              // chunks entirely inside the buffer
+    auto chunk_at = [&](int64_t w0) -> const uint32_t * {   // clamped aligned chunk
+        int64_t c = w0 / CW;
+        c = c < 0 ? 0 : (c >= full ? full - 1 : c);
+        return p.in + c * CW;
+    };
+
+    // ---- loads: up (aligned part + next lane), centre, down (aligned part + next lane)
+    uint32_t u0[CW], cm[CW], d0[CW], un[CW], dn[CW];
+    const int64_t au = (int64_t)base - S - RU;        // multiple of CW
+    const int64_t ad = (int64_t)base + S - RD;
+    flat_load<CW>(chunk_at(au), u0);
+    flat_load<CW>(chunk_at(base), cm);
+    flat_load<CW>(chunk_at(ad), d0);
+    // lane 31's successor chunks (the next warp's lane 0)
+    if (lane == 31) {
+        flat_load<CW>(chunk_at(au + CW), un);
+        flat_load<CW>(chunk_at(ad + CW), dn);
+    }
+    uint32_t lwm = 0, rwm = 0;                        // memory words before / after the chunk
+    if (lane == 0 && base > 0) lwm = __ldg(p.in + base - 1);
+    if (lane == 31 && base + CW < p.nwords) rwm = __ldg(p.in + base + CW);
+
+    // up[j] = flat word base - S + j (memory order) = (u0 ++ next lane's u0)[RU + j]
+    uint32_t up[CW], dw[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+        if (j + RU < CW) {
+            up[j] = u0[j + RU];
+        } else {
+            const uint32_t x = __shfl_down_sync(0xFFFFFFFFu, u0[j + RU - CW], 1);
+            up[j] = lane == 31 ? un[j + RU - CW] : x;
+        }
+        if (j + RD < CW) {
+            dw[j] = d0[j + RD];
+        } else {
+            const uint32_t x = __shfl_down_sync(0xFFFFFFFFu, d0[j + RD - CW], 1);
+            dw[j] = lane == 31 ? dn[j + RD - CW] : x;
+        }
+    }
+
+    // ---- chunks whose clamped vector loads may not cover what they need: the first
+    // and last two rows' worth of chunks and the ragged tail -- reload word by word
+    const bool edge_zone = base < S + 2 * CW || base + S + 2 * CW > p.nwords ||
+                           base + CW > p.nwords;
+    if (edge_zone) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            const int64_t f = (int64_t)base + j;
+            cm[j] = f < p.nwords ? __ldg(p.in + f) : 0u;
+            up[j] = f - S >= 0 && f - S < p.nwords ? __ldg(p.in + f - S) : 0u;
+            dw[j] = f + S < p.nwords ? __ldg(p.in + f + S) : 0u;
+        }
+    }
+
+    // ---- pixel order (uint64 rows swap each pair) and horizontal neighbours
+    uint32_t cc[CW], cu[CW], cd[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+        cc[j] = cm[j ^ SWAP];
+        cu[j] = up[j ^ SWAP];
+        cd[j] = dw[j ^ SWAP];
+    }
+    // pixel-order word before the chunk: lane-1's last; after: lane+1's first
+    uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cc[CW - 1], 1);
+    uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
+    if (lane == 0) {
+        // pixel word base-1 is memory word base-1 (u32) or base-2 (u64 pair)
+        lw = SWAP ? (base >= 2 ? __ldg(p.in + base - 2) : 0u) : lwm;
+    }
+    if (lane == 31) {
+        rw = SWAP ? (base + CW + 1 < p.nwords ? __ldg(p.in + base + CW + 1) : 0u) : rwm;
+    }
+    if (!live) return;
+
+    // ---- row / column of the chunk's first word; words past the row end wrap
+    const uint32_t r0 = fdiv(base, p.div_s);
+    const uint32_t c0 = base - r0 * S;
+    const uint32_t y0 = r0 - fdiv(r0, p.div_h) * p.h;
+    const uint32_t fw = p.fillword;
+    uint32_t ve[CW], vs[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+        uint32_t c = c0 + j, y = y0;
+        if (c >= S) {                                 // S >= 2 * CW: at most one wrap
+            c -= S;
+            y = (y0 + 1 == p.h) ? 0 : y0 + 1;
+        }
+        const uint32_t left = j == 0 ? lw : cc[j - 1];
+        const uint32_t right = j == CW - 1 ? rw : cc[j + 1];
+        uint32_t ln = __funnelshift_r(cc[j], c == 0 ? fw : left, 1);
+        uint32_t rn = __funnelshift_l(right, cc[j], 1);
+        const uint32_t u = y == 0 ? fw : cu[j];
+        const uint32_t d = y == p.h - 1 ? fw : cd[j];
+        uint32_t f = 0u;
+        if ((int)c == p.pl) {
+            rn = (rn & ~p.lastbit) | (fw & p.lastbit);
+            f = p.padmask;
+        } else if ((int)c > p.pl) {
+            f = 0xFFFFFFFFu;
+        }
+        const uint32_t a = ln | rn | u | d;
+        ve[j ^ SWAP] = cc[j] | ~a | f;
+        vs[j ^ SWAP] = (~cc[j] & a) | f;
+    }
+    if (base + CW <= p.nwords) {
+        if (OUT != kOutEset) store_chunk<CW>(p.o_edges + base, ve);
+        if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + base, vs);
+    } else {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            if (base + j < p.nwords) {
+                if (OUT != kOutEset) p.o_edges[base + j] = ve[j];
+                if (OUT != kOutEdges) p.o_eset[base + j] = vs[j];
+            }
+        }
+    }
+}
+
+}  // namespace bitedge
