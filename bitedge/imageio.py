@@ -1,3 +1,5 @@
-"""`bitedge.imageio` PBM part (reference: SPEC.md:273-316, module not shipped) -> B200
-implementation with the P4 payload decoded/encoded on the device (PGM is out of scope)."""
-from paper_1401_5245_b200.pbm import detect_pbm, parse_header, read_pbm, write_pbm  # noqa: F401
+"""`bitedge.imageio` (reference: SPEC.md:273-316, module not shipped) -> B200
+implementation: PBM with the P4 payload decoded/encoded on the device, and the
+PGM reader (host-side header + payload parse)."""
+from paper_1401_5245_b200.pbm import (  # noqa: F401
+    detect_pbm, parse_header, read_pbm, read_pgm, write_pbm)

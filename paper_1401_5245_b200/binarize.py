@@ -55,20 +55,29 @@ def threshold_edges(gray, t: int, border: BorderPolicy = BorderPolicy.WHITE_OUTS
 
 def otsu_threshold(gray: np.ndarray) -> int:
     """Between-class-variance maximiser over the 256-bin histogram; ties go to the
-    smaller threshold.  Histogram on the device."""
+    smaller threshold.  The histogram is counted on the
+    device; the 256 candidates are then compared EXACTLY on the host in integer
+    arithmetic: for threshold t (black class = samples < t) with class counts
+    w0, w1 and sample sums s0, s1, the variance w0*w1*(s0/w0 - s1/w1)^2 equals
+    (s0*w1 - s1*w0)^2 / (w0*w1), and two candidates compare by cross-
+    multiplication -- no floating-point near-ties."""
     torch = _torch()
     g = _gray_tensor(gray).reshape(-1)
-    hist = torch.bincount(g.to(torch.int64), minlength=256).to(torch.float64)
-    total = hist.sum()
-    t = torch.arange(256, dtype=torch.float64, device=g.device)
-    w0 = torch.cumsum(hist, 0) - hist             # samples < t  (black class for threshold t)
-    m0 = torch.cumsum(hist * t, 0) - hist * t
-    w1 = total - w0
-    m1 = (hist * t).sum() - m0
-    valid = (w0 > 0) & (w1 > 0)
-    var = torch.where(valid, w0 * w1 * (m0 / w0.clamp(min=1) - m1 / w1.clamp(min=1)) ** 2,
-                      torch.zeros_like(w0))
-    best = var.max()
-    if best <= 0:
-        return 0
-    return int(torch.nonzero(var >= best * (1 - 1e-12))[0].item())
+    hist = [int(v) for v in torch.bincount(g.to(torch.int64), minlength=256).tolist()]
+    total = sum(hist)
+    total_sum = sum(t * c for t, c in enumerate(hist))
+    best_t, best_num, best_den = 0, 0, 1            # variance 0 at t = 0 (w0 = 0)
+    w0 = s0 = 0
+    for t in range(256):
+        # class 0 = samples < t
+        if t > 0:
+            w0 += hist[t - 1]
+            s0 += (t - 1) * hist[t - 1]
+        w1, s1 = total - w0, total_sum - s0
+        if w0 == 0 or w1 == 0:
+            continue
+        num = (s0 * w1 - s1 * w0) ** 2
+        den = w0 * w1
+        if num * best_den > best_num * den:          # strictly larger: ties keep the smaller t
+            best_t, best_num, best_den = t, num, den
+    return best_t

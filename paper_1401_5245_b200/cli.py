@@ -30,6 +30,7 @@ class CliError(Exception):
 
 
 from .binarize import otsu_threshold  # noqa: E402,F401  (re-exported for the CLI)
+from .pbm import read_pgm  # noqa: E402,F401  (imageio.read_pgm; re-exported for the CLI)
 
 
 def _read(path: str) -> bytes:
@@ -73,43 +74,6 @@ def _bool(s: str) -> bool:
 
 
 # ---------------------------------------------------------------- PGM (binarize input)
-
-def read_pgm(data: bytes):
-    """P2 / P5 with maxval <= 255 -> uint8 array."""
-    if len(data) < 2 or data[:1] != b"P" or data[1:2] not in (b"2", b"5"):
-        raise ValueError("not a PGM file (magic P2/P5 expected) at offset 0")
-    magic = data[1:2]
-    pos, vals = 2, []
-    while len(vals) < 3:
-        while pos < len(data) and (data[pos:pos + 1].isspace() or data[pos:pos + 1] == b"#"):
-            if data[pos:pos + 1] == b"#":
-                while pos < len(data) and data[pos] not in b"\r\n":
-                    pos += 1
-            else:
-                pos += 1
-        start = pos
-        while pos < len(data) and data[pos:pos + 1].isdigit():
-            pos += 1
-        if start == pos:
-            raise ValueError(f"malformed PGM header at offset {start}")
-        vals.append(int(data[start:pos]))
-    w, h, maxval = vals
-    if w < 1 or h < 1:
-        raise ValueError("image dimensions must be at least 1x1")
-    if maxval > 255:
-        raise ValueError(f"maxval {maxval} > 255 not supported (offset {pos})")
-    pos += 1
-    if magic == b"5":
-        need = w * h
-        if len(data) - pos < need:
-            raise ValueError(f"short PGM payload: need {need} bytes at offset {pos}, "
-                             f"have {len(data) - pos}")
-        return np.frombuffer(data[pos:pos + need], np.uint8).reshape(h, w).copy()
-    toks = data[pos:].split()
-    if len(toks) < w * h:
-        raise ValueError(f"short PGM payload: need {w * h} samples after offset {pos}")
-    return np.array([int(t) for t in toks[: w * h]], np.uint8).reshape(h, w)
-
 
 # ---------------------------------------------------------------- bench shapes
 

@@ -124,7 +124,20 @@ class HostBatchEdges:
         # Lanes past the first are allocated on first use.
         self._lanes = [(self.streams, self._din, self._dout)]
         self._keep = [self.d_in, self.d_out]
+        self._adopt(self.streams, self.d_in + self.d_out)
         self._next = 0
+
+    def _adopt(self, streams, bufs) -> None:
+        """Hand caching-allocator blocks (allocated on the current stream) to the
+        lane streams: the lane streams start after whatever the current stream
+        queued before (the blocks may have been reused memory), and the blocks are
+        recorded on them so the allocator never recycles one while a lane's copy
+        or kernel is still queued."""
+        cur = torch.cuda.current_stream(self.device)
+        for st in streams:
+            st.wait_stream(cur)
+            for t in bufs:
+                t.record_stream(st)
 
     def _lane(self, k: int):
         if k >= len(self._lanes):
@@ -132,8 +145,9 @@ class HostBatchEdges:
             d_out = [torch.empty_like(t) for t in self.d_out]
             self._keep += [d_in, d_out]
             P = ctypes.c_void_p
-            self._lanes.append(([torch.cuda.Stream(self.device) for _ in range(2)],
-                                (P * 2)(*[t.data_ptr() for t in d_in]),
+            streams = [torch.cuda.Stream(self.device) for _ in range(2)]
+            self._adopt(streams, d_in + d_out)
+            self._lanes.append((streams, (P * 2)(*[t.data_ptr() for t in d_in]),
                                 (P * 2)(*[t.data_ptr() for t in d_out])))
         return self._lanes[k]
 
@@ -219,15 +233,17 @@ class HostBatchEdges:
             e = torch.cuda.Event()
             e.record(s_)
             evs.append(e)
-        return Pending(evs, host_out)
+        return Pending(evs, host_out, self)
 
 
 class Pending:
-    """A submitted host batch (`HostBatchEdges.submit`)."""
+    """A submitted host batch (`HostBatchEdges.submit`).  Holds the pipe (and so
+    its device buffers) until the batch is done."""
 
-    def __init__(self, events, host_out):
+    def __init__(self, events, host_out, owner=None):
         self._events = events
         self.host_out = host_out
+        self._owner = owner
 
     def query(self) -> bool:
         return all(e.query() for e in self._events)

@@ -142,3 +142,44 @@ def detect_pbm(data: bytes, border: BorderPolicy = BorderPolicy.WHITE_OUTSIDE,
     from .edge import detect_edges_mask
 
     return write_pbm(detect_edges_mask(read_pbm(data), border), raw)
+
+
+def read_pgm(data: bytes):
+    """`imageio.read_pgm` (SPEC.md:293-301): P2 / P5 with maxval <= 255 -> the
+    samples verbatim as a uint8 array [H, W] (the GrayImage the binarize
+    functions take); maxval > 255 and short payloads raise ValueError with the
+    byte offset.  Host-side parsing: PGM is the photograph entry point, not
+    part of the edge path."""
+    if len(data) < 2 or data[:1] != b"P" or data[1:2] not in (b"2", b"5"):
+        raise ValueError("not a PGM file (magic P2/P5 expected) at offset 0")
+    magic = data[1:2]
+    pos, vals = 2, []
+    while len(vals) < 3:
+        while pos < len(data) and (data[pos:pos + 1].isspace() or data[pos:pos + 1] == b"#"):
+            if data[pos:pos + 1] == b"#":
+                while pos < len(data) and data[pos] not in b"\r\n":
+                    pos += 1
+            else:
+                pos += 1
+        start = pos
+        while pos < len(data) and data[pos:pos + 1].isdigit():
+            pos += 1
+        if start == pos:
+            raise ValueError(f"malformed PGM header at offset {start}")
+        vals.append(int(data[start:pos]))
+    w, h, maxval = vals
+    if w < 1 or h < 1:
+        raise ValueError("image dimensions must be at least 1x1")
+    if maxval > 255:
+        raise ValueError(f"maxval {maxval} > 255 not supported (offset {pos})")
+    pos += 1
+    if magic == b"5":
+        need = w * h
+        if len(data) - pos < need:
+            raise ValueError(f"short PGM payload: need {need} bytes at offset {pos}, "
+                             f"have {len(data) - pos}")
+        return np.frombuffer(data[pos:pos + need], np.uint8).reshape(h, w).copy()
+    toks = data[pos:].split()
+    if len(toks) < w * h:
+        raise ValueError(f"short PGM payload: need {w * h} samples after offset {pos}")
+    return np.array([int(t) for t in toks[: w * h]], np.uint8).reshape(h, w)

@@ -144,3 +144,40 @@ def test_binarize_properties(cuda_dev):
             assert t == min(u for u in range(256) if abs(var(u) - best) <= 1e-9 * best)
         else:
             assert t == 0
+
+
+def _otsu_exact(img):
+    """Brute force with exact rationals: the smallest t attaining the maximum
+    between-class variance w0*w1*(mean0 - mean1)^2."""
+    from fractions import Fraction
+
+    x = [int(v) for v in np.asarray(img).reshape(-1)]
+    best, arg = Fraction(0), 0
+    for t in range(256):
+        lo = [v for v in x if v < t]
+        hi = [v for v in x if v >= t]
+        if not lo or not hi:
+            continue
+        v = len(lo) * len(hi) * (Fraction(sum(lo), len(lo)) - Fraction(sum(hi), len(hi))) ** 2
+        if v > best:
+            best, arg = v, t
+    return arg
+
+
+def test_otsu_exact_ties(cuda_dev):
+    """Exact tie-breaking (a float tolerance could pick a smaller,
+    non-maximal t): symmetric histograms with exact ties, and random images."""
+    from paper_1401_5245_b200.binarize import otsu_threshold
+
+    rng = np.random.default_rng(11)
+    cases = [np.array([[0, 255]], np.uint8),
+             np.array([[10, 10, 200, 200]], np.uint8),
+             np.array([[0, 100, 155, 255]], np.uint8),                 # symmetric: ties
+             np.array([[3, 4, 250, 251, 3, 251]], np.uint8),
+             np.full((3, 3), 0, np.uint8), np.full((3, 3), 255, np.uint8)]
+    for _ in range(12):
+        k = int(rng.integers(2, 6))
+        vals = rng.choice(256, k, replace=False)
+        cases.append(rng.choice(vals, (int(rng.integers(1, 40)), 3)).astype(np.uint8))
+    for img in cases:
+        assert otsu_threshold(img) == _otsu_exact(img), img.reshape(-1)[:12]
