@@ -368,6 +368,47 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const int groups = (int)(G.h / rpi);
             const int64_t nimg = G.n;
             const int64_t grid = (nimg * 32 + kThreads - 1) / kThreads;
+            // K2p: the whole batch requested by TMA at kernel start, one CTA per SM
+            // (up to IPW images of <= 8 KB per warp); K2w otherwise
+            constexpr int kIPW = 4;
+            const int64_t img_bytes = (int64_t)groups * 1024;
+            const int64_t warps_needed = (nimg + kIPW - 1) / kIPW;
+            const int64_t cta = (warps_needed + 7) / 8;
+            const int64_t ctas = cta < sm_count() ? sm_count() : cta;
+            const int64_t nwarps = ctas * 8 < nimg ? ctas * 8 : nimg;
+            const size_t psmem = 128 + (size_t)8 * kIPW * img_bytes;
+            if (!knob(KN_NO_K2P) && nimg >= 8 && psmem <= 227 * 1024 &&
+                ((uintptr_t)in % 16) == 0 && nimg < ((int64_t)1 << 40)) {
+                const unsigned pgrid = (unsigned)((nwarps + 7) / 8);
+#define BE_K2P(L)                                                                              \
+    case L: {                                                                                  \
+        auto kern = o_edges && o_eset ? edge_warp_img_tma_kernel<L, kOutAny, kIPW>              \
+                  : o_eset ? edge_warp_img_tma_kernel<L, kOutEset, kIPW>                       \
+                           : edge_warp_img_tma_kernel<L, kOutEdges, kIPW>;                     \
+        static bool attr_set = false;                                                          \
+        if (!attr_set) {                                                                       \
+            cudaFuncSetAttribute(edge_warp_img_tma_kernel<L, kOutAny, kIPW>,                    \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);      \
+            cudaFuncSetAttribute(edge_warp_img_tma_kernel<L, kOutEset, kIPW>,                   \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);      \
+            cudaFuncSetAttribute(edge_warp_img_tma_kernel<L, kOutEdges, kIPW>,                  \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);      \
+            attr_set = true;                                                                   \
+        }                                                                                      \
+        launch_kb(kern, pgrid, (unsigned)kThreads, psmem, st, rp, groups, nimg, nwarps);       \
+        return cuda_check("edge_warp_img_tma_kernel");                                         \
+    }
+                switch (lwpr) {
+                    BE_K2P(0)
+                    BE_K2P(1)
+                    BE_K2P(2)
+                    BE_K2P(3)
+                    BE_K2P(4)
+                    BE_K2P(5)
+                    default: break;
+                }
+#undef BE_K2P
+            }
             if (grid <= 0x7FFFFFFFLL) {
 #define BE_WARPIMG_G(L, GM)                                                                    \
     do {                                                                                       \

@@ -50,6 +50,7 @@ enum Knob : int {
     KN_P4_BYTES,
     KN_PDL,
     KN_NO_FLAT,
+    KN_NO_K2P,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

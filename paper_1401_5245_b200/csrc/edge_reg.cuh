@@ -759,6 +759,91 @@ __device__ __forceinline__ void wtma(void *dst, const void *src, uint32_t bytes,
         : "memory");
 }
 
+// K2p: the K2w batch shape (small uint8 images, one warp per image) with the
+// whole batch requested from DRAM at kernel start.  K2w issues each image's
+// loads from registers, so a batch is 1.15 waves at C2 and the last 15 % of
+// images start a full load latency late; here every warp's lane 0 issues one
+// `cp.async.bulk` (TMA) per image it owns into shared memory -- up to
+// IPW images per warp, the CTA's 8 warps holding <= 8 * IPW * G KB -- each
+// tracked by its own mbarrier, so with one CTA per SM all ~16 MiB of C2 are in
+// flight at once; each warp then computes its images in arrival order with
+// K2w's register math, reading its lane's 32 bytes of each row group from
+// shared memory.  Warps get a balanced contiguous range of images (global warp
+// gw owns images [gw*N/W, (gw+1)*N/W)).
+template <int LWPR, int OUT, int IPW>
+__global__ void __launch_bounds__(kThreads, 1)
+edge_warp_img_tma_kernel(const RegParams p, int G, int64_t nimg, int64_t nwarps) {
+    extern __shared__ __align__(128) unsigned char k2p_smem[];
+    constexpr int WPR = 1 << LWPR;
+    constexpr int RPI = 32 >> LWPR;
+    constexpr int WARPS = kThreads / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+    const int64_t i0 = gw * nimg / nwarps, i1 = (gw + 1) * nimg / nwarps;
+    const int cnt = (int)(i1 - i0);                        // <= IPW (host sizes nwarps)
+    const uint32_t img_bytes = (uint32_t)G * 1024u;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(k2p_smem) + warp * IPW;
+    unsigned char *buf = k2p_smem + 128 + (size_t)warp * IPW * img_bytes;
+    if (lane == 0) {
+        for (int k = 0; k < cnt; ++k) wbar_init(&bars[k]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    if (lane == 0) {
+        for (int k = 0; k < cnt; ++k) {
+            wbar_expect(&bars[k], img_bytes);
+            wtma(buf + (size_t)k * img_bytes, p.in + (i0 + k) * (int64_t)img_bytes, img_bytes,
+                 &bars[k]);
+        }
+    }
+    const Thr T = make_thr(p.thr);
+    const int rl = lane >> LWPR, wi = lane & (WPR - 1);
+    const uint32_t fw = p.fillword;
+    const bool last_word = (wi == WPR - 1);
+    for (int k = 0; k < cnt; ++k) {
+        wbar_wait(&bars[k], 0);
+        const unsigned char *src = buf + (size_t)k * img_bytes + 32 * lane;
+        uint32_t wd[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g < G) {
+                const uint4 a = *reinterpret_cast<const uint4 *>(src + 1024 * g);
+                const uint4 b = *reinterpret_cast<const uint4 *>(src + 1024 * g + 16);
+                wd[g] = pack32_any(a, b, T);
+            } else {
+                wd[g] = 0xFFFFFFFFu;
+            }
+        }
+        const int64_t img = i0 + k;
+        uint32_t *oe = p.o_edges + img * (int64_t)G * 32 + lane;
+        uint32_t *os = p.o_eset + img * (int64_t)G * 32 + lane;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= G) break;
+            const uint32_t cw = wd[g];
+            const uint32_t up_in = __shfl_up_sync(0xFFFFFFFFu, cw, WPR);
+            const uint32_t dn_in = __shfl_down_sync(0xFFFFFFFFu, cw, WPR);
+            const uint32_t up_x = __shfl_sync(0xFFFFFFFFu, g > 0 ? wd[g > 0 ? g - 1 : 0] : fw,
+                                              (lane + 32 - WPR) & 31);
+            const uint32_t dn_x = __shfl_sync(0xFFFFFFFFu, g + 1 < G ? wd[g + 1 < 8 ? g + 1 : 7] : fw,
+                                              (lane + WPR) & 31);
+            const uint32_t u = rl > 0 ? up_in : (g > 0 ? up_x : fw);
+            const uint32_t d = rl < RPI - 1 ? dn_in : (g + 1 < G ? dn_x : fw);
+            uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cw, 1);
+            const uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cw, 1);
+            if (wi == 0) lw = fw;
+            const uint32_t ln = __funnelshift_r(cw, lw, 1);
+            uint32_t rn = __funnelshift_l(rw, cw, 1);
+            if (last_word) rn = (rn & ~1u) | (fw & 1u);   // pixel w-1 reads the fill
+            const uint32_t any = ln | rn | u | d;
+            if (OUT != kOutEset) __stcs(oe + 32 * g, cw | ~any);
+            if (OUT != kOutEdges) __stcs(os + 32 * g, ~cw & any);
+        }
+    }
+}
+
 // One warp owns a 1024-pixel row segment (32 output words, one per lane) of a
 // strip of RSL rows.  Its lane 0 streams the strip's RSL+2 staged rows (the
 // segment plus 16 bytes either side for the neighbour pixels) into a private

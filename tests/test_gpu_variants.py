@@ -1,12 +1,14 @@
 """Every kernel variant the C ABI can dispatch to must agree bit-for-bit with
-the per-pixel oracle.  The library reads its selection knobs from the
-environment at each call, so one process can exercise them all:
+the per-pixel oracle.  One process exercises them all through the library's
+selection knobs:
 
     default        register-direct kernels (K1 8/4-word items, K2 one-shot
                    strips, K2r rolling strips, K2w warp-per-image)
     tile           one-shot shared-memory tile kernel (the general fallback)
     stream         persistent TMA (cp.async.bulk + mbarrier) pipelined kernel
-    cw4, rs8, no_roll, no_warpimg, no_pdl   individual knobs
+    cw4, rs8, no_roll, no_warpimg, no_pdl, no_k2p, no_flat   individual knobs
+(the knobs are read once per process; tests/conftest.py re-reads them after
+every monkeypatch.setenv)
 """
 
 import numpy as np
@@ -39,11 +41,14 @@ VARIANTS = {
     "unal_chunks": {"BITEDGE_UNAL_CHUNKS": "1"},
     "unal_bytes": {"BITEDGE_UNAL_BYTES": "1"},
     "u64_tma": {"BITEDGE_U64_TMA": "1"},
+    "no_k2p": {"BITEDGE_NO_K2P": "1"},
+    "no_flat": {"BITEDGE_NO_FLAT": "1"},
 }
 
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
 SHAPES = [(64, 64, 64), (8, 32, 32), (3, 40, 2048), (2, 70, 4160), (5, 33, 100), (1, 1, 1), (3, 50, 8000), (2, 9, 1000),
-          (1, 300, 1), (1, 1, 700), (4, 16, 256), (2, 200, 8192)]
+          (1, 300, 1), (1, 1, 700), (4, 16, 256), (2, 200, 8192), (1500, 32, 32),
+          (600, 16, 64), (333, 64, 128)]
 
 
 def _t(a, dev):
