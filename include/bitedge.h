@@ -100,6 +100,16 @@ int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
                             int64_t row_stride_words, int fill_bit, int64_t row_lo, int64_t row_hi,
                             void *stream);
 
+/* K3e: output rows 0 and rows-1 of a slab only (the two rows that read a halo),
+ * in one launch; same arguments and meaning as be_edge_packed_halo_u32 with the
+ * row range fixed to {0, rows-1}.  Row-sharded callers compute rows
+ * [1, rows-1) with be_edge_packed_halo_u32 while the halo rows are exchanged,
+ * then this.  (Replaces, for the boundary rows, the vertical fill the
+ * reference applies at rows 0 / H-1: bitimage.py:216-223.) */
+int be_edge_packed_halo_ends_u32(const uint32_t *slab, const uint32_t *above_or_null,
+                                 const uint32_t *below_or_null, uint32_t *out, int64_t rows,
+                                 int64_t w, int64_t row_stride_words, int fill_bit, void *stream);
+
 /* General form of K1/K2/K3 with every optional output (F3 of SURVEY 8(f)).
  * input_kind 0: packed words of `word_bits`; 1: uint8 pixels (in_row_stride
  * in bytes).  above/below as in K3 (n must be 1 when either is non-NULL). */

@@ -35,6 +35,7 @@ _SIGNATURES = {
     "be_edge_packed_u64": [_P, _P, _I64, _I64, _I64, _I64, _INT, _INT, _P],
     "be_pack_edge_u8": [_P, _P, _I64, _I64, _I64, _I64, _I64, _INT, _P, _P],
     "be_edge_packed_halo_u32": [_P, _P, _P, _P, _I64, _I64, _I64, _INT, _I64, _I64, _P],
+    "be_edge_packed_halo_ends_u32": [_P, _P, _P, _P, _I64, _I64, _I64, _INT, _P],
     "be_edges_general": [_P, _INT, _I64, _P, _P, ctypes.POINTER(be_outputs), _INT, _I64, _I64,
                          _I64, _I64, _INT, _I64, _I64, _P],
     "be_pack_u8": [_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _P],

@@ -697,6 +697,43 @@ int edges_impl(const void *in, int input_kind, int64_t in_stride, const void *ab
     return vec ? launch_tile<kU8Vec>(tp, rows, st) : launch_tile<kU8Byte>(tp, rows, st);
 }
 
+
+// K3e: output rows 0 and rows-1 of a row slab -- the only two rows that read a
+// halo -- in ONE launch (row-sharded C4: the interior rows
+// [1, rows-1) run in K1 while the halo rows are in flight, then this kernel
+// finishes the slab).  Thread = one uint32 word of one of the two rows; the
+// up / down rows come from the slab or the halo row (NULL: the border fill,
+// bitimage.py:216-223), the left / right neighbour words straight from the row
+// (pixel w-1's right neighbour is the fill, bitimage.py:235-239); padding = 1.
+__global__ void __launch_bounds__(256)
+edge_halo_ends_kernel(const uint32_t *__restrict__ slab, const uint32_t *__restrict__ above,
+                      const uint32_t *__restrict__ below, uint32_t *__restrict__ out,
+                      int64_t rows, int64_t stride, int wp, int pl, uint32_t lastbit,
+                      uint32_t padmask, uint32_t fw) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nends = rows > 1 ? 2 : 1;
+    if (t >= (int64_t)nends * wp) return;
+    const int which = (int)(t / wp);
+    const int j = (int)(t - (int64_t)which * wp);
+    const int64_t r = which == 0 ? 0 : rows - 1;
+    const uint32_t *row = slab + r * stride;
+    const uint32_t c = row[j];
+    const uint32_t lw = j > 0 ? row[j - 1] : fw;
+    const uint32_t rw = j + 1 < wp ? row[j + 1] : fw;
+    const uint32_t u = r > 0 ? row[j - stride] : (above ? above[j] : fw);
+    const uint32_t d = r + 1 < rows ? row[j + stride] : (below ? below[j] : fw);
+    const uint32_t ln = __funnelshift_r(c, lw, 1);
+    uint32_t rn = __funnelshift_l(rw, c, 1);
+    uint32_t f = 0u;
+    if (j == pl) {
+        rn = (rn & ~lastbit) | (fw & lastbit);
+        f = padmask;
+    }
+    out[r * stride + j] = c | ~(ln | rn | u | d) | f;
+}
+
 }  // namespace capi
 }  // namespace bitedge
 
@@ -751,6 +788,24 @@ int be_edge_packed_halo_u32(const uint32_t *slab, const uint32_t *above_or_null,
     if (out == nullptr) return fail(BE_EINVAL, "output is NULL");
     return edges_impl(slab, 0, row_stride_words, above_or_null, below_or_null, out, nullptr, side,
                       nullptr, 32, row_stride_words, 1, rows, w, fill_bit, row_lo, row_hi, stream);
+}
+
+int be_edge_packed_halo_ends_u32(const uint32_t *slab, const uint32_t *above_or_null,
+                                 const uint32_t *below_or_null, uint32_t *out, int64_t rows,
+                                 int64_t w, int64_t row_stride_words, int fill_bit, void *stream) {
+    Geometry G;
+    int rc = make_geometry(G, 32, 1, rows, w, fill_bit);
+    if (rc) return rc;
+    if ((rc = check_stride(G, row_stride_words, "row"))) return rc;
+    if ((rc = check_ptr(slab, 32, "slab"))) return rc;
+    if ((rc = check_ptr(out, 32, "output"))) return rc;
+    if ((above_or_null && ((uintptr_t)above_or_null & 3)) || (below_or_null && ((uintptr_t)below_or_null & 3)))
+        return fail(BE_EALIGN, "halo rows must be 4-byte aligned");
+    const int64_t total = (rows > 1 ? 2 : 1) * (int64_t)G.wp;
+    launch_kb(edge_halo_ends_kernel, (unsigned)((total + 255) / 256), 256u, 0, S(stream), slab,
+              above_or_null, below_or_null, out, rows, row_stride_words, G.wp, G.pl, G.lastbit,
+              G.padmask, G.fillword);
+    return cuda_check("edge_halo_ends_kernel");
 }
 
 int be_pack_u8(const uint8_t *in, void *out, int word_bits, int64_t n, int64_t h, int64_t w,

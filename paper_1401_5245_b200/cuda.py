@@ -525,6 +525,27 @@ def edges_halo(slab: torch.Tensor, above, below, width: int, border=WHITE_OUTSID
     return o
 
 
+def edges_halo_ends(slab: torch.Tensor, above, below, width: int, border=WHITE_OUTSIDE, *,
+                    out) -> torch.Tensor:
+    """Kernel K3e: output rows 0 and rows-1 of a row slab only -- the two rows
+    that read a halo -- in one launch (`edges_halo` with the rows {0, rows-1});
+    `out` must already hold (or later receive) the interior rows."""
+    _require_cuda(slab, "slab")
+    if slab.dim() != 2 or word_bits_of(slab) != 32:
+        raise ValueError("slab must be a 2-d 32-bit word tensor")
+    w3, wb, rs = _packed(slab, width, "slab")
+    for t, nm in ((above, "above"), (below, "below")):
+        if t is not None:
+            _require_cuda(t, nm)
+            if t.dtype != slab.dtype or t.numel() < slab.shape[1] or t.stride(-1) != 1:
+                raise ValueError(f"{nm} must be one contiguous row of the slab's dtype")
+    if out.shape != slab.shape or out.dtype != slab.dtype or out.stride() != slab.stride():
+        raise ValueError("out must match the slab")
+    _capi.call("be_edge_packed_halo_ends_u32", _ptr(slab), _ptr(above), _ptr(below), _ptr(out),
+               slab.shape[0], int(width), rs, fill_bit(border), _stream(slab))
+    return out
+
+
 # ------------------------------------------------------------------ primitives
 
 def pack_u8(pixels: torch.Tensor, word_bits: int = 32, out=None) -> torch.Tensor:

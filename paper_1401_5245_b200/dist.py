@@ -103,10 +103,13 @@ class RowShardedEdges:
     `slab` is an int32 CUDA tensor [rows, S] of MSB-first row words; the
     result lands in `self.out` (same shape)."""
 
-    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None, compute=None):
+    def __init__(self, slab: torch.Tensor, width: int, border=1, group=None, compute=None,
+                 compute_ends=None):
         """`compute(slab, above, below, out, row_lo, row_hi)` computes output rows
-        [row_lo, row_hi) of the slab; the default is kernel K3 through the C ABI
-        (the CPU tests substitute the oracle to exercise this orchestration)."""
+        [row_lo, row_hi) of the slab (default: kernel K3 through the C ABI) and
+        `compute_ends(slab, above, below, out)` its rows 0 and rows-1 (default:
+        K3e, one launch for both); the CPU tests substitute the oracle for both
+        to exercise this orchestration."""
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.group = group
@@ -126,7 +129,13 @@ class RowShardedEdges:
             def compute(sl, ab, be, out, lo, hi):
                 _cuda.edges_halo(sl, ab, be, self.width, self.border, out=out, row_lo=lo,
                                  row_hi=hi)
+        if compute_ends is None:
+            from . import cuda as _cuda
+
+            def compute_ends(sl, ab, be, out):
+                _cuda.edges_halo_ends(sl, ab, be, self.width, self.border, out=out)
         self.compute = compute
+        self.compute_ends = compute_ends
 
     def step(self) -> torch.Tensor:
         rows, s = self.rows, self.slab.shape[1]
@@ -141,9 +150,7 @@ class RowShardedEdges:
             self.compute(self.slab, None, None, self.out, 1, rows - 1)
         for w in works:
             w.wait()
-        self.compute(self.slab, above, below, self.out, 0, 1)
-        if rows > 1:
-            self.compute(self.slab, above, below, self.out, rows - 1, rows)
+        self.compute_ends(self.slab, above, below, self.out)   # rows 0 and rows-1
         return self.out
 
 

@@ -96,15 +96,28 @@ def _worker_rowshard(rank, world, port, H, W, seed, q):
             full = cscan.scan_p32_slab(sl.numpy().view(np.uint32), a, b, W, 1)
             out[r0:r1] = torch.from_numpy(full[r0:r1].view(np.int32))
 
-        rs = RowShardedEdges(slab, W, 1, compute=oracle_k3)
+        def oracle_k3e(sl, ab, be, out):
+            n = sl.shape[0]
+            calls.append(("ends", ab is not None, be is not None))
+            a = None if ab is None else ab.numpy().view(np.uint32)[: sl.shape[1]]
+            b = None if be is None else be.numpy().view(np.uint32)[: sl.shape[1]]
+            full = cscan.scan_p32_slab(sl.numpy().view(np.uint32), a, b, W, 1)
+            out[0] = torch.from_numpy(full[0].view(np.int32))
+            out[n - 1] = torch.from_numpy(full[n - 1].view(np.int32))
+
+        rs = RowShardedEdges(slab, W, 1, compute=oracle_k3, compute_ends=oracle_k3e)
         out = rs.step().numpy().view(np.uint32).copy()
         obj = [None] * world
-        dist.all_gather_object(obj, (lo, out, calls))
+        dist.all_gather_object(obj, (rank, lo, out, calls))
         if rank == 0:
-            full = np.concatenate([o[1] for o in sorted(obj, key=lambda t: t[0])])
+            obj.sort(key=lambda t: t[1])
+            full = np.concatenate([o[2] for o in obj])
             ok = bool((full == cscan.scan_p32(packed, W, 1)).all())
-            # interior first, without halos; boundary rows after, with them
-            ok &= all(c[0][2:] == (False, False) for _, _, c in obj if len(c) > 1)
+            # interior rows [1, n-1) first, without halos; then ONE call for rows
+            # 0 and n-1 with the halos that exist at this rank's position
+            for r, _, o, c in obj:
+                ok &= len(c) == 2 and c[0] == (1, len(o) - 1, False, False) and c[1] == (
+                    "ends", r > 0, r < world - 1)
             q.put(ok)
     finally:
         dist.destroy_process_group()

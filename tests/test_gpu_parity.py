@@ -424,6 +424,41 @@ def test_row_slabs_with_halos_equal_whole(cuda_dev, G, W, prs, monkeypatch):
         assert torch.equal(torch.cat(parts), whole), (G, fill)
 
 
+@pytest.mark.parametrize("W", [1, 31, 32, 33, 100, 1000, 8192, 65536])
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_row_slabs_halo_ends_kernel(cuda_dev, G, W):
+    """RowShardedEdges' schedule: K3 on the interior rows [1, n-1), then K3e
+    (rows 0 and n-1, one launch) with the received halos -- equal to the whole
+    raster; K3e writes nothing but those two rows (sentinel), n = 1 and 2
+    included."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(W + G)
+    H = 2 * G + 3 if W > 8192 else 61
+    a = (rng.random((H, W)) < 0.5).astype(np.uint8)
+    pk = torch.from_numpy(P.pack_u32(a).view(np.int32)).to(cuda_dev)
+    cuts = [0, 1, 3] + list(np.linspace(4, H, G - 1).astype(int)) if G >= 3 else [0, 1, H]
+    cuts = sorted(set(int(c) for c in cuts))
+    for fill in (1, 0):
+        whole = cu.pack_edges_u8(_t(a, cuda_dev), fill)
+        parts = []
+        for r in range(len(cuts) - 1):
+            lo, hi = cuts[r], cuts[r + 1]
+            n = hi - lo
+            slab = pk[lo:hi].clone()
+            above = pk[lo - 1].clone() if lo > 0 else None
+            below = pk[hi].clone() if hi < H else None
+            out = torch.full_like(slab, 0x5A5A5A5A)
+            cu.edges_halo_ends(slab, above, below, W, fill, out=out)
+            if n > 2:
+                assert (out[1:n - 1] == 0x5A5A5A5A).all(), "K3e wrote an interior row"
+                cu.edges_halo(slab, None, None, W, fill, out=out, row_lo=1, row_hi=n - 1)
+            parts.append(out)
+        assert torch.equal(torch.cat(parts), whole), (G, W, fill, cuts)
+
+
 @pytest.mark.parametrize("zc", [False, True, None])     # staged copies / kernel over host memory / auto
 def test_host_pipeline_e2e(cuda_dev, zc):
     from paper_1401_5245_b200 import synth
