@@ -12,7 +12,8 @@ with no distributed code; this layer is new.
   ordered by a device-side step-counter handshake (stream memory operations).
   `RowShardedEdges`: one packed row to each row neighbour by grouped NCCL
   send/recv (8 KiB per message at 65536 px) while the interior rows, which need
-  no halo, are computed; then the two boundary rows with the received halos.
+  no halo, are computed; the two boundary rows follow the received halos on a
+  side stream (one K3e launch), overlapping the interior kernel.
 """
 
 from __future__ import annotations
@@ -136,6 +137,7 @@ class RowShardedEdges:
                 _cuda.edges_halo_ends(sl, ab, be, self.width, self.border, out=out)
         self.compute = compute
         self.compute_ends = compute_ends
+        self._side = None
 
     def step(self) -> torch.Tensor:
         rows, s = self.rows, self.slab.shape[1]
@@ -146,11 +148,26 @@ class RowShardedEdges:
         if self.world == 1:
             self.compute(self.slab, None, None, self.out, 0, rows)
             return self.out
+        cuda = self.slab.is_cuda
+        if cuda:
+            # the two end rows on a side stream behind the exchange, so they
+            # overlap the interior kernel instead of following it
+            cur = torch.cuda.current_stream(self.slab.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream(self.slab.device)
+            self._side.wait_stream(cur)
+            with torch.cuda.stream(self._side):
+                for w in works:
+                    w.wait()
+                self.compute_ends(self.slab, above, below, self.out)   # rows 0 and rows-1
         if rows > 2:  # interior rows need no halo: overlap them with the exchange
             self.compute(self.slab, None, None, self.out, 1, rows - 1)
-        for w in works:
-            w.wait()
-        self.compute_ends(self.slab, above, below, self.out)   # rows 0 and rows-1
+        if cuda:
+            cur.wait_stream(self._side)
+        else:
+            for w in works:
+                w.wait()
+            self.compute_ends(self.slab, above, below, self.out)
         return self.out
 
 

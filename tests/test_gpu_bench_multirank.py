@@ -5,6 +5,7 @@ numbers of such a run mean nothing; the real multi-GPU run is the driver's."""
 
 import json
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -23,6 +24,21 @@ def _port():
     return p
 
 
+def _run_group(cmd, env, timeout):
+    """Run torchrun in its own process group and kill the WHOLE group on timeout
+    (a plain subprocess timeout would kill torchrun only and leave its ranks
+    running on the GPU)."""
+    p = subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                         text=True, start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, err = p.communicate()
+        pytest.fail(f"timed out after {timeout} s: {' '.join(cmd[-8:])}\n{err[-4000:]}")
+    return subprocess.CompletedProcess(cmd, p.returncode, out, err)
+
+
 @pytest.mark.parametrize("extra", [["--config", "c2", "--steps", "300"],
                                    ["--config", "c2", "--steps", "300", "--weak"],
                                    ["--config", "c4", "--steps", "4"],
@@ -36,8 +52,8 @@ def test_bench_two_ranks_one_gpu(extra, cuda_dev):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
            "--warmup", "3", "--no-dropin", *extra]
-    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
-    assert res.returncode == 0, res.stderr[-2000:]
+    res = _run_group(cmd, env, timeout=300)
+    assert res.returncode == 0, res.stderr[-4000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, res.stdout
     d = json.loads(lines[0])
