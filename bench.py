@@ -59,7 +59,7 @@ DTYPE = "u32"        # both arms: bitwise arithmetic on packed row words
 DEFAULT_STEPS = {"c1": 200000, "c2": 200000, "c3": 150000, "c4": 3000, "c5": 600}
 
 
-SPACER_CYCLES = 1_000_000          # ~0.5 ms at 1.965 GHz (row-sharded per-iteration timing)
+SPACER_CYCLES = 1_000_000          # ~0.5 ms device spacer at 1.965 GHz before a timed region
 
 
 def log(*a):
@@ -504,6 +504,7 @@ def run_ours(args):
                 gs.replay()
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(SPACER_CYCLES)     # the replay is submitted while this runs
                 a.record()
                 gs.replay()
                 b.record()
@@ -532,6 +533,7 @@ def run_ours(args):
                 run(1, 1)
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(SPACER_CYCLES)
                 a.record()
                 run(n_s, 1)
                 b.record()
@@ -599,6 +601,10 @@ def run_ours(args):
                   "queue behind, CUDA events around each iteration, max over ranks per iteration")
     else:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # the K steps' launches (a graph replay, or direct launches) are submitted
+        # while a ~0.5 ms device spacer runs, so the events time the device work
+        # of the K steps rather than the host's submission latency
+        torch.cuda._sleep(SPACER_CYCLES)
         ev0.record()
         run(steps)
         ev1.record()
@@ -609,7 +615,8 @@ def run_ours(args):
             t = torch.tensor([ms_rank], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_max = float(t.item())
-        timing = "barrier, CUDA events around the K steps, max over ranks"
+        timing = ("barrier, then a 0.5 ms device spacer the K steps' launches queue behind, "
+                  "CUDA events around the K steps, max over ranks")
     t_wall1 = time.time()
     if world > 1:
         dist.barrier()

@@ -192,16 +192,6 @@ int be_ipc_export(const void *dev_ptr, void *handle_out, int64_t *offset_out);
 int be_ipc_open(const void *handle, int64_t offset, void **dev_ptr_out);
 int be_ipc_close(void *dev_ptr, int64_t offset);
 
-/* Per-step producer -> consumer handshake of the peer halos, on the device: each
- * rank publishes 32-bit step counters ("my slab of step s is complete", "I have
- * finished reading my neighbours' rows of step s") in a small IPC-exported
- * device buffer; be_stream_write32 enqueues the write of `value` to `flag` after
- * all prior work on `stream` (with a memory barrier), be_stream_wait_geq32
- * makes `stream` wait until *flag >= value (flag: device or IPC peer memory,
- * 4-byte aligned).  Stream memory operations: no kernel spins, no host round
- * trip.  (No reference counterpart: the reference is single-process numpy.) */
-int be_stream_wait_geq32(const void *flag, uint32_t value, void *stream);
-int be_stream_write32(void *flag, uint32_t value, void *stream);
 
 /* ---- host buffers (the end-to-end path) ----------------------------------- */
 

@@ -53,8 +53,6 @@ _SIGNATURES = {
     "be_ipc_export": [_P, _P, ctypes.POINTER(_I64)],
     "be_ipc_open": [_P, _I64, ctypes.POINTER(_P)],
     "be_ipc_close": [_P, _I64],
-    "be_stream_wait_geq32": [_P, ctypes.c_uint32, _P],
-    "be_stream_write32": [_P, ctypes.c_uint32, _P],
     "be_host_edges": [_P, _INT, _P, _I64, _I64, _I64, _INT, ctypes.POINTER(_P),
                       ctypes.POINTER(_P), _I64, _P, _P, _INT],
     "be_host_edges_rows": [_P, _INT, _P, _I64, _I64, _INT, _INT, ctypes.POINTER(_P),

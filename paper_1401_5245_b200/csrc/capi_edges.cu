@@ -376,8 +376,11 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
             const int64_t cta = (warps_needed + 7) / 8;
             const int64_t ctas = cta < sm_count() ? sm_count() : cta;
             const int64_t nwarps = ctas * 8 < nimg ? ctas * 8 : nimg;
-            const size_t psmem = 128 + (size_t)8 * kIPW * img_bytes;
-            if (!knob(KN_NO_K2P) && nimg >= 8 && psmem <= 227 * 1024 &&
+            // barrier header (8 warps x kIPW mbarriers, 128-byte rounded) + buffers;
+            // must match edge_warp_img_tma_kernel's HDR
+            const size_t psmem = (size_t)((8 * kIPW * 8 + 127) / 128 * 128) +
+                                 (size_t)8 * kIPW * img_bytes;
+            if (knob(KN_K2P) && nimg >= 8 && psmem <= 227 * 1024 &&
                 ((uintptr_t)in % 16) == 0 && nimg < ((int64_t)1 << 40)) {
                 const unsigned pgrid = (unsigned)((nwarps + 7) / 8);
 #define BE_K2P(L)                                                                              \

@@ -23,7 +23,7 @@ const char *const kKnobNames[KN_COUNT] = {
     "BITEDGE_NO_WARPIMG", "BITEDGE_WARPIMG_G4", "BITEDGE_PDL_LATE", "BITEDGE_TMA1",
     "BITEDGE_FORCE_TMA", "BITEDGE_U64_TMA", "BITEDGE_TMA2_RSL8", "BITEDGE_TMA2_RSL32",
     "BITEDGE_NO_ROLL", "BITEDGE_RS", "BITEDGE_PRS", "BITEDGE_UNAL_RS4", "BITEDGE_P4_UNFUSED",
-    "BITEDGE_P4_BYTES", "BITEDGE_PDL", "BITEDGE_NO_FLAT", "BITEDGE_NO_K2P"};
+    "BITEDGE_P4_BYTES", "BITEDGE_PDL", "BITEDGE_NO_FLAT", "BITEDGE_K2P", "BITEDGE_SYNC_BLOCK"};
 }  // namespace capi
 }  // namespace bitedge
 
@@ -110,46 +110,6 @@ int be_ipc_close(void *dev_ptr, int64_t offset) {
     return BE_OK;
 }
 
-// ---- device-side producer -> consumer handshake for peer halos -------------
-// Stream memory operations (cuStreamWaitValue32 / cuStreamWriteValue32, looked up
-// through the runtime's driver entry point so the library does not link libcuda):
-// the GPU front end waits for / writes a 32-bit word in device or IPC peer memory
-// in stream order -- no kernel spins, no host round trip.
-typedef int (*cuStreamWaitValue32_t)(void *, unsigned long long, uint32_t, unsigned int);
-typedef int (*cuStreamWriteValue32_t)(void *, unsigned long long, uint32_t, unsigned int);
-
-static void *driver_fn(const char *name) {
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-        return nullptr;
-    return fn;
-}
-
-int be_stream_wait_geq32(const void *flag, uint32_t value, void *stream) {
-    if (flag == nullptr) return fail(BE_EINVAL, "NULL flag");
-    if (((uintptr_t)flag & 3) != 0) return fail(BE_EINVAL, "flag must be 4-byte aligned");
-    static cuStreamWaitValue32_t fn = (cuStreamWaitValue32_t)driver_fn("cuStreamWaitValue32");
-    if (fn == nullptr) return fail(BE_EINVAL, "cuStreamWaitValue32 unavailable");
-    // CU_STREAM_WAIT_VALUE_GEQ = 0: (int32_t)(*flag - value) >= 0
-    int r = fn(stream, (unsigned long long)(uintptr_t)flag, value, 0x0);
-    if (r != 0) return fail(r, "cuStreamWaitValue32 failed (CUresult %d)", r);
-    return BE_OK;
-}
-
-int be_stream_write32(void *flag, uint32_t value, void *stream) {
-    if (flag == nullptr) return fail(BE_EINVAL, "NULL flag");
-    if (((uintptr_t)flag & 3) != 0) return fail(BE_EINVAL, "flag must be 4-byte aligned");
-    static cuStreamWriteValue32_t fn = (cuStreamWriteValue32_t)driver_fn("cuStreamWriteValue32");
-    if (fn == nullptr) return fail(BE_EINVAL, "cuStreamWriteValue32 unavailable");
-    // CU_STREAM_WRITE_VALUE_DEFAULT = 0: ordered after (and with a memory barrier
-    // behind) all prior work on the stream
-    int r = fn(stream, (unsigned long long)(uintptr_t)flag, value, 0x0);
-    if (r != 0) return fail(r, "cuStreamWriteValue32 failed (CUresult %d)", r);
-    return BE_OK;
-}
-
 int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64_t n, int64_t h,
                   int64_t w, int fill_bit, void *const dev_in[2], uint32_t *const dev_out[2],
                   int64_t chunk_images, void *stream0, void *stream1, int blocking) {
@@ -192,6 +152,25 @@ int be_host_edges(const void *host_in, int input_kind, uint32_t *host_out, int64
         }
     }
     return BE_OK;
+}
+
+// Completion wait of the drop-in's one-call flows (a few microseconds of GPU
+// work per call, then the host reads the result): spin on an event query rather
+// than cudaStreamSynchronize, whose wake-up under the default scheduling mode
+// cost ~6 us of the ~15 us C1/C2 call on the B200 box (scripts/dropin_breakdown.py).
+// BITEDGE_SYNC_BLOCK=1 restores cudaStreamSynchronize (A/B).
+static cudaError_t wait_stream_spin(cudaStream_t st) {
+    if (knob(KN_SYNC_BLOCK)) return cudaStreamSynchronize(st);
+    thread_local cudaEvent_t ev = nullptr;
+    if (ev == nullptr) {
+        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ev, st);
+    if (e != cudaSuccess) return e;
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    }
+    return e;
 }
 
 int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_bit,
@@ -239,7 +218,7 @@ int be_host_detect_u64(const uint8_t *host_pix, int64_t h, int64_t w, int fill_b
                                         cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) return fail((int)e, "D2H: %s", cudaGetErrorString(e));
     }
-    cudaError_t e = cudaStreamSynchronize(st);
+    cudaError_t e = wait_stream_spin(st);
     if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
     return BE_OK;
 }
@@ -291,7 +270,7 @@ int be_host_detect_u64_staged(const uint8_t *pix, int64_t pix_row_stride, int64_
                     st);
     if (rc) return rc;
     if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[2]);
-    cudaError_t e = cudaStreamSynchronize(st);
+    cudaError_t e = wait_stream_spin(st);
     if (e != cudaSuccess) return fail((int)e, "sync: %s", cudaGetErrorString(e));
     if (trace) clock_gettime(CLOCK_MONOTONIC, &ts[3]);
     memcpy(words_out, stage_out, (size_t)(h * wp * 8));

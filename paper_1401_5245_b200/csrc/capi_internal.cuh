@@ -50,7 +50,8 @@ enum Knob : int {
     KN_P4_BYTES,
     KN_PDL,
     KN_NO_FLAT,
-    KN_NO_K2P,
+    KN_K2P,
+    KN_SYNC_BLOCK,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

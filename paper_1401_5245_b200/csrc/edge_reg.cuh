@@ -779,11 +779,15 @@ edge_warp_img_tma_kernel(const RegParams p, int G, int64_t nimg, int64_t nwarps)
     constexpr int WARPS = kThreads / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+    if (gw >= nwarps) return;                              // whole warp (no CTA barriers)
     const int64_t i0 = gw * nimg / nwarps, i1 = (gw + 1) * nimg / nwarps;
     const int cnt = (int)(i1 - i0);                        // <= IPW (host sizes nwarps)
     const uint32_t img_bytes = (uint32_t)G * 1024u;
+    // [mbarriers of all warps | image buffers]: the header holds WARPS * IPW
+    // barriers, rounded up to 128 bytes (k2p_smem_bytes on the host)
+    constexpr int HDR = (WARPS * IPW * 8 + 127) / 128 * 128;
     uint64_t *bars = reinterpret_cast<uint64_t *>(k2p_smem) + warp * IPW;
-    unsigned char *buf = k2p_smem + 128 + (size_t)warp * IPW * img_bytes;
+    unsigned char *buf = k2p_smem + HDR + (size_t)warp * IPW * img_bytes;
     if (lane == 0) {
         for (int k = 0; k < cnt; ++k) wbar_init(&bars[k]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

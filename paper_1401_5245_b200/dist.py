@@ -7,9 +7,9 @@ with no distributed code; this layer is new.
   the data path.
 * Row sharding (config C4): rank r owns rows [lo, hi) of one giant raster;
   ranks 0 and G-1 use the border fill on their outer side (bitimage.py:216-223).
-  `PeerHaloEdges`: the edge kernel reads the neighbours' boundary rows straight
-  from their HBM over NVLink (CUDA IPC peer pointers) -- one launch per step,
-  ordered by a device-side step-counter handshake (stream memory operations).
+  `PeerHaloEdges` (opt-in): the edge kernel reads the neighbours' boundary rows
+  straight from their HBM over NVLink (CUDA IPC peer pointers) -- one launch
+  per step, ordered by a host-side handshake (stream sync + barrier).
   `RowShardedEdges`: one packed row to each row neighbour by grouped NCCL
   send/recv (8 KiB per message at 65536 px) while the interior rows, which need
   no halo, are computed; the two boundary rows follow the received halos on a
@@ -201,28 +201,27 @@ class PeerHaloEdges:
     """Row-sharded edges whose halo rows are read from the neighbour ranks'
     slabs over NVLink by the edge kernel itself (CUDA IPC peer pointers passed
     as K3's `above` / `below`): no exchange step and one kernel per step -- the
-    fused alternative to `RowShardedEdges`' NCCL send/recv.
+    fused alternative to `RowShardedEdges`' NCCL send/recv (opt-in:
+    bench.py --halo p2p).
 
-    Setup exports this rank's slab and a small step-counter buffer
-    (`be_ipc_export`), all-gathers the handles and opens the row neighbours'
-    (`be_ipc_open`).  Every step runs a device-side producer -> consumer
-    handshake in stream order (`be_stream_write32` / `be_stream_wait_geq32`,
-    stream memory operations on the counters -- no host round trip, no
-    spinning kernel):
+    Setup exports this rank's slab (`be_ipc_export`), all-gathers the handles
+    and opens the row neighbours' (`be_ipc_open`).  Ordering between ranks is a
+    host-side handshake on the process group -- no kernel and no stream waits
+    on another rank's memory:
 
-        step():  ready[me] := s       this rank's slab of step s is complete
-                 wait ready[above] >= s and ready[below] >= s
-                 edge kernel (reads the neighbours' boundary rows)
-                 done[me] := s        finished reading the neighbours' rows
+        step():               this rank's stream is synchronised (its slab of
+                              step s is complete), then a barrier (every
+                              neighbour's is), then the edge kernel
+        acquire_for_write():  this rank's stream is synchronised (its kernel
+                              has finished reading the neighbours' rows), then
+                              a barrier -- call before overwriting the slab, so
+                              no neighbour still reads step s's boundary rows.
 
-        acquire_for_write():  wait done[above] >= s and done[below] >= s
-                 -- call before overwriting the slab for step s + 1, so no
-                 neighbour still reads step s's boundary rows.
-
-    The slab must be written on the current stream (or ordered before it)
-    before step()."""
-
-    READY, DONE = 0, 16          # counter word offsets (separate 64-byte lines)
+    (A device-side handshake with stream memory operations on IPC-shared
+    counters was tried: on this driver a stream waiting on a counter that
+    another stream writes never resumed, even inside one process -- DESIGN.md
+    section 6.)  The slab must be written on the current stream before
+    step()."""
 
     def __init__(self, slab: torch.Tensor, width: int, border=1, group=None):
         import ctypes
@@ -230,6 +229,7 @@ class PeerHaloEdges:
         from . import _capi
 
         self._capi, self._ct = _capi, ctypes
+        self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         if slab.dim() != 2 or slab.dtype != torch.int32 or not slab.is_cuda or \
@@ -238,24 +238,19 @@ class PeerHaloEdges:
         self.slab, self.width, self.border = slab, int(width), border
         self.rows, self.stride = slab.shape[0], slab.stride(0)
         self.out = torch.empty_like(slab)
-        self.flags = torch.zeros(32, dtype=torch.int32, device=slab.device)
-        self.s = 0
-        torch.cuda.synchronize(slab.device)        # counters are zero before anyone waits
-        mine = (self._export(slab), self._export(self.flags), self.rows, self.stride)
+        self._opened = []
+        self.above_ptr = self.below_ptr = None
+        mine = (self._export(slab), self.rows, self.stride)
         everyone = [None] * self.world
         everyone[self.rank] = mine
         if self.world > 1:
             dist.all_gather_object(everyone, mine, group=group)
-        self._opened = []
-        self.above_ptr = self.above_flags = self.below_ptr = self.below_flags = None
         if self.rank > 0:
-            (h, off), (fh, foff), rows, stride = everyone[self.rank - 1]
+            (h, off), rows, stride = everyone[self.rank - 1]
             self.above_ptr = self._open(h, off) + (rows - 1) * stride * 4
-            self.above_flags = self._open(fh, foff)
         if self.rank < self.world - 1:
-            (h, off), (fh, foff), _, _ = everyone[self.rank + 1]
+            (h, off), _, _ = everyone[self.rank + 1]
             self.below_ptr = self._open(h, off)
-            self.below_flags = self._open(fh, foff)
 
     def _export(self, t: torch.Tensor):
         ct = self._ct
@@ -269,42 +264,27 @@ class PeerHaloEdges:
         self._opened.append(handle)
         return ptr
 
-    def _stream(self):
-        return self._ct.c_void_p(torch.cuda.current_stream(self.slab.device).cuda_stream)
-
-    def _wait(self, flags_ptr, word, value, st):
-        if flags_ptr is not None:
-            self._capi.call("be_stream_wait_geq32", self._ct.c_void_p(flags_ptr + 4 * word),
-                            value, st)
-
-    def _publish(self, word, value, st):
-        self._capi.call("be_stream_write32", self._ct.c_void_p(self.flags.data_ptr() + 4 * word),
-                        value, st)
+    def _sync_all(self) -> None:
+        if self.world > 1:
+            torch.cuda.current_stream(self.slab.device).synchronize()
+            dist.barrier(group=self.group)
 
     def acquire_for_write(self) -> None:
-        """Order the current stream after the neighbours' reads of this slab's
-        step-s boundary rows (call before rewriting the slab)."""
-        st = self._stream()
-        self._wait(self.above_flags, self.DONE, self.s, st)
-        self._wait(self.below_flags, self.DONE, self.s, st)
+        """Return once every rank's kernel has finished reading its neighbours'
+        rows (call before rewriting the slab)."""
+        self._sync_all()
 
     def step(self) -> torch.Tensor:
         ct = self._ct
         from . import cuda as cu
 
-        self.s += 1
-        st = self._stream()
-        if self.world > 1:
-            self._publish(self.READY, self.s, st)
-            self._wait(self.above_flags, self.READY, self.s, st)
-            self._wait(self.below_flags, self.READY, self.s, st)
+        self._sync_all()                   # every slab of this step is complete
+        st = ct.c_void_p(torch.cuda.current_stream(self.slab.device).cuda_stream)
         self._capi.call("be_edge_packed_halo_u32", ct.c_void_p(self.slab.data_ptr()),
                         ct.c_void_p(self.above_ptr) if self.above_ptr else None,
                         ct.c_void_p(self.below_ptr) if self.below_ptr else None,
                         ct.c_void_p(self.out.data_ptr()), self.rows, self.width, self.stride,
                         cu.fill_bit(self.border), 0, self.rows, st)
-        if self.world > 1:
-            self._publish(self.DONE, self.s, st)
         return self.out
 
     def close(self):

@@ -9,6 +9,7 @@ import signal
 import socket
 import subprocess
 import sys
+import time
 
 import pytest
 
@@ -24,19 +25,36 @@ def _port():
     return p
 
 
-def _run_group(cmd, env, timeout):
-    """Run torchrun in its own process group and kill the WHOLE group on timeout
-    (a plain subprocess timeout would kill torchrun only and leave its ranks
-    running on the GPU)."""
-    p = subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
-                         text=True, start_new_session=True)
+def _run_ranks(args, env, world, timeout):
+    """Launch the `world` ranks of `python bench.py args` directly (what torchrun
+    does: RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* in the environment), each in
+    its own session, and kill every rank on timeout -- torchrun starts its
+    workers in new sessions, so killing a timed-out torchrun would leave its
+    ranks running on the GPU.  Returns rank 0's CompletedProcess; the other
+    ranks' stderr is appended to it on failure."""
+    port = str(_port())
+    procs = []
+    for r in range(world):
+        e = dict(env, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(world), LOCAL_WORLD_SIZE=str(world),
+                 MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+        procs.append(subprocess.Popen([sys.executable, "bench.py", *args], cwd=ROOT, env=e,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                                      start_new_session=True))
+    deadline = time.time() + timeout
+    outs = []
     try:
-        out, err = p.communicate(timeout=timeout)
+        for p in procs:
+            outs.append(p.communicate(timeout=max(1.0, deadline - time.time())))
     except subprocess.TimeoutExpired:
-        os.killpg(p.pid, signal.SIGKILL)
-        out, err = p.communicate()
-        pytest.fail(f"timed out after {timeout} s: {' '.join(cmd[-8:])}\n{err[-4000:]}")
-    return subprocess.CompletedProcess(cmd, p.returncode, out, err)
+        for p in procs:
+            if p.poll() is None:
+                os.killpg(p.pid, signal.SIGKILL)
+        errs = [p.communicate()[1] for p in procs]
+        pytest.fail(f"timed out after {timeout} s: bench.py {' '.join(args)}\n" +
+                    "\n".join(e[-2000:] for e in errs))
+    rc = max(p.returncode for p in procs)
+    err = "\n".join(f"[rank {r}] {o[1][-2000:]}" for r, o in enumerate(outs)) if rc else outs[0][1]
+    return subprocess.CompletedProcess(args, rc, outs[0][0], err)
 
 
 @pytest.mark.parametrize("extra", [["--config", "c2", "--steps", "300"],
@@ -49,10 +67,7 @@ def test_bench_two_ranks_one_gpu(extra, cuda_dev):
     NCCL (rows staged through the host); p2p runs the IPC peer reads with the
     device-side handshake."""
     env = dict(os.environ, BITEDGE_SHARE_GPU="1", BITEDGE_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--warmup", "3", "--no-dropin", *extra]
-    res = _run_group(cmd, env, timeout=300)
+    res = _run_ranks(["--gpus", "2", "--warmup", "3", "--no-dropin", *extra], env, 2, timeout=300)
     assert res.returncode == 0, res.stderr[-4000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, res.stdout

@@ -172,3 +172,83 @@ def test_p4_guards(w, G, cuda_dev):
     out = host[G: G + n * h * rb].reshape(n, h, rb)
     got = 1 - np.unpackbits(out, axis=-1)[..., :w]
     assert (got == P.unpack_u32(cscan.scan_u8(a, 1), w)).all()
+
+
+@pytest.mark.parametrize("n,h,w", [(8, 64, 64), (9, 64, 64), (100, 32, 32), (333, 64, 128),
+                                   (1183, 64, 64), (1185, 48, 64), (4096, 64, 64),
+                                   (5000, 32, 64), (700, 224, 32)])
+def test_k2p_guarded_batches(cuda_dev, n, h, w, monkeypatch):
+    """K2p (opt-in, BITEDGE_K2P: whole glyph batch requested by TMA at kernel
+    start, one CTA per SM):
+    image counts that are not multiples of the warp count, mbarrier header and
+    image buffers side by side in shared memory -- output bit-exact, nothing
+    written past the batch (guard words), EdgeSet too."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    monkeypatch.setenv("BITEDGE_K2P", "1")
+    rng = np.random.default_rng(n * 7 + h)
+    a = (rng.random((n, h, w)) < 0.6).astype(np.uint8)
+    # garbage bytes after the last image (a warp reading a nonexistent image
+    # would pick them up and write their edges into the guard words)
+    src = torch.from_numpy(np.concatenate([a.reshape(-1), rng.integers(0, 256, 64 * 1024,
+                                                                        dtype=np.uint8)]))
+    x = src.to(cuda_dev)[: a.size].view(n, h, w)
+    wp = -(-w // 32)
+    for fill in (1, 0):
+        for eset in (False, True):
+            buf = torch.full((n * h * wp + 2 * GUARD,), SENT, dtype=torch.int32, device=cuda_dev)
+            view = buf[GUARD: GUARD + n * h * wp].view(n, h, wp)
+            if eset:
+                cu.edges_general(x, w, fill, edges=False, edgeset=True, outs={"edgeset": view})
+            else:
+                cu.pack_edges_u8(x, fill, out=view)
+            torch.cuda.synchronize()
+            b = buf.cpu().numpy()
+            assert (b[:GUARD] == SENT).all() and (b[GUARD + n * h * wp:] == SENT).all()
+            exp = cscan.scan_u8(a, fill, edgeset=eset)
+            assert (view.cpu().numpy().view(np.uint32) == exp).all(), (n, h, w, fill, eset)
+
+
+@pytest.mark.parametrize("k2p", ["0", "1"])
+def test_glyph_batches_concurrent_streams(cuda_dev, k2p, monkeypatch):
+    """The bench's schedule (K2w by default, K2p opt-in): C2 batches on three parallel streams (CUDA graph
+    replay, PDL between consecutive launches of a stream), distinct outputs,
+    every output bit-exact."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+    from paper_1401_5245_b200 import synth
+
+    if k2p == "1":
+        monkeypatch.setenv("BITEDGE_K2P", "1")
+    imgs = synth.c2_images(4096)
+    exp = cscan.scan_u8(imgs.numpy(), 1)
+    x = imgs.to(cuda_dev)
+    outs = [torch.empty((4096, 64, 2), dtype=torch.int32, device=cuda_dev) for _ in range(24)]
+    side = [torch.cuda.Stream(cuda_dev) for _ in range(3)]
+    g = torch.cuda.CUDAGraph()
+    cur = torch.cuda.current_stream(cuda_dev)
+    for s_ in side:
+        s_.wait_stream(cur)
+    with torch.cuda.stream(side[0]):
+        cu.pack_edges_u8(x, 1, out=outs[0])             # warm-up outside the capture
+    cur.wait_stream(side[0])
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        c = torch.cuda.current_stream(cuda_dev)
+        for s_ in side:
+            s_.wait_stream(c)
+        for i in range(len(outs)):
+            with torch.cuda.stream(side[i % 3]):
+                cu.pack_edges_u8(x, 1, out=outs[i])
+        for s_ in side:
+            c.wait_stream(s_)
+    for _ in range(20):
+        for o in outs:
+            o.fill_(0)
+        g.replay()
+        torch.cuda.synchronize()
+        for o in outs:
+            assert (o.cpu().numpy().view(np.uint32) == exp).all()

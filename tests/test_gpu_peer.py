@@ -1,9 +1,10 @@
-"""Peer-memory halos (PeerHaloEdges): two or three ranks on ONE GPU exchange
-CUDA IPC handles over gloo and each runs a single edge kernel that reads its
-neighbour's boundary row straight from the other process's allocation; on an
-8-GPU box the same pointers resolve over NVLink.  No kernel waits on another:
-the per-step handshake is stream memory operations on IPC-shared counters,
-which the GPU front end resolves (a blocked stream holds no SM)."""
+"""Peer-memory halos (PeerHaloEdges, bench.py --halo p2p): two or three ranks
+on ONE GPU exchange CUDA IPC handles over gloo and each runs a single edge
+kernel that reads its neighbour's boundary row straight from the other
+process's allocation; on an 8-GPU box the same pointers resolve over NVLink.
+The per-step handshake is host-side (stream synchronize + barrier), so no
+kernel and no stream waits on another process's memory -- processes that wait
+on one another on the device must not share a GPU (B200_PROFILING.md)."""
 
 import os
 import socket
@@ -38,14 +39,11 @@ def _worker(rank, world, port, H, W, q):
         packed = P.pack_u32(img)
         lo, hi = shard_range(H, rank, world)
         slab = torch.from_numpy(packed[lo:hi].view(np.int32).copy()).cuda()
-        torch.cuda.synchronize()
         ph = PeerHaloEdges(slab, W, 1)
-        dist.barrier()                      # every slab is in HBM before anyone reads it
         out = ph.step().cpu().numpy().view(np.uint32)
-        torch.cuda.synchronize()
         exp = cscan.scan_p32(packed, W, 1)[lo:hi]
         ok = bool((out == exp).all())
-        dist.barrier()                      # neighbours done reading before memory goes away
+        ph.acquire_for_write()              # neighbours done reading before memory goes away
         ph.close()
         res = [None] * world
         dist.all_gather_object(res, ok)
@@ -56,7 +54,7 @@ def _worker(rank, world, port, H, W, q):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_peer_halo_two_processes_one_gpu(world, cuda_dev):
+def test_peer_halo_processes_one_gpu(world, cuda_dev):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     mp.spawn(_worker, args=(world, _port(), 150, 8192, q), nprocs=world, join=True)
@@ -83,9 +81,7 @@ def _worker_rewrite(rank, world, port, H, W, steps, q):
             rasters.append(P.pack_u32(img))
         src = torch.from_numpy(np.stack([r[lo:hi] for r in rasters]).view(np.int32)).cuda()
         slab = torch.zeros_like(src[0])
-        torch.cuda.synchronize()
         ph = PeerHaloEdges(slab, W, 1)
-        dist.barrier()
         outs = []
         for k in range(steps):
             ph.acquire_for_write()              # neighbours are done with step k-1's rows
@@ -98,7 +94,7 @@ def _worker_rewrite(rank, world, port, H, W, steps, q):
         for k in range(steps):
             exp = cscan.scan_p32(rasters[k], W, 1)[lo:hi]
             ok &= bool((outs[k].cpu().numpy().view(np.uint32) == exp).all())
-        dist.barrier()
+        ph.acquire_for_write()
         ph.close()
         res = [None] * world
         dist.all_gather_object(res, ok)

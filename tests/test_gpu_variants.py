@@ -6,7 +6,7 @@ selection knobs:
                    strips, K2r rolling strips, K2w warp-per-image)
     tile           one-shot shared-memory tile kernel (the general fallback)
     stream         persistent TMA (cp.async.bulk + mbarrier) pipelined kernel
-    cw4, rs8, no_roll, no_warpimg, no_pdl, no_k2p, no_flat   individual knobs
+    cw4, rs8, no_roll, no_warpimg, no_pdl, k2p, no_flat   individual knobs
 (the knobs are read once per process; tests/conftest.py re-reads them after
 every monkeypatch.setenv)
 """
@@ -41,7 +41,7 @@ VARIANTS = {
     "unal_chunks": {"BITEDGE_UNAL_CHUNKS": "1"},
     "unal_bytes": {"BITEDGE_UNAL_BYTES": "1"},
     "u64_tma": {"BITEDGE_U64_TMA": "1"},
-    "no_k2p": {"BITEDGE_NO_K2P": "1"},
+    "k2p": {"BITEDGE_K2P": "1"},
     "no_flat": {"BITEDGE_NO_FLAT": "1"},
 }
 
