@@ -88,6 +88,16 @@ int launch_reg_packed(RegParams &rp, int swap, int cw, int rs, unsigned grid, cu
             return cuda_check("edge_reg_packed_kernel<UNAL>");
         }
     }
+    if constexpr (OUT != kOutAll) {
+        if (rp.h16) {                                      // 16-byte rows, 8-word items
+            if (cw != 8 || (rs != 2 && rs != 4)) return kNoKernel;
+            if (swap && rs == 2) launch_k(edge_reg_packed_kernel<1, 2, 8, OUT, HALO, false, false, false, true>, grid, 0, st, rp, dv);
+            else if (swap) launch_k(edge_reg_packed_kernel<1, 4, 8, OUT, HALO, false, false, false, true>, grid, 0, st, rp, dv);
+            else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 8, OUT, HALO, false, false, false, true>, grid, 0, st, rp, dv);
+            else launch_k(edge_reg_packed_kernel<0, 4, 8, OUT, HALO, false, false, false, true>, grid, 0, st, rp, dv);
+            return cuda_check("edge_reg_packed_kernel<H16>");
+        }
+    }
     if constexpr (OUT == kOutAll) {   // up to 7 outputs: 4-word items keep it in registers
         if (swap) launch_k(edge_reg_packed_kernel<1, 4, 4, OUT, HALO>, grid, 0, st, rp, dv);
         else if (rs == 2) launch_k(edge_reg_packed_kernel<0, 2, 4, OUT, HALO>, grid, 0, st, rp, dv);
@@ -338,6 +348,15 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     const int64_t strips4 = (row_hi - row_lo + 3) / 4;
     const bool big = strips4 * ((G.wp + 7) / 8) >= (int64_t)sm_count() * 4096;
     int cw = (input_kind == 0 && in32 && !multi && !knob(KN_CW4)) ? 8 : 4;
+    // rows that are 16-byte but not 32-byte multiples: 8-word items as two 128-bit
+    // loads / stores (H16) instead of 4-word items (8192 x 8000 uint64 words:
+    // the per-item work over 8 words, not 4)
+    const bool in16 = al16(in) && in_row_bytes % 16 == 0 && al16(above) && al16(below);
+    if (input_kind == 0 && !in32 && in16 && !unal && !multi && !knob(KN_CW4) &&
+        !knob(KN_NO_H16)) {
+        cw = 8;
+        rp.h16 = 1;
+    }
     if (unal) {
         if (multi) return kNoKernel;
         // contiguous rows (stride == row length): the flat kernel's aligned vector
@@ -350,13 +369,13 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         rp.unal_words = knob(KN_UNAL_CHUNKS) == nullptr;   // words: measured faster
     }
     // (uint64 words take 2-row strips only in the tail-free and UNAL kernels)
-    const bool swap2 = !G.swap || unal || k1_aligned(!multi, cw, G.w);
+    const bool swap2 = !G.swap || unal || rp.h16 || k1_aligned(!multi, cw, G.w);
     const int packed_rs = (input_kind == 0 && swap2 && !big) ? 2 : 4;
     if (input_kind == 0 && in32 && !multi && knob(KN_CW8)) cw = 8;
     rp.items = input_kind == 1 ? G.wp : (G.wp + cw - 1) / cw;
     rp.v8 = input_kind == 1 && in32 && G.w % 32 == 0;
     rp.thr = thr;
-    const int ocw = input_kind == 1 ? 1 : cw;
+    const int ocw = input_kind == 1 ? 1 : rp.h16 ? 4 : cw;
     rp.vst = (out_stride_u32 % ocw == 0) && al(o_edges, 4 * ocw) && al(o_eset, 4 * ocw);
     for (int k = 0; k < 4; ++k) rp.vst = rp.vst && al(o_side[k], 4 * ocw);
     rp.vst = rp.vst && al(o_packed, 4 * ocw);
@@ -535,7 +554,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         const char *rse = knob(KN_PRS);      // packed strip height experiments: 2/4/8
         if (rse) rs = atoi(rse) == 2 ? 2 : (atoi(rse) == 8 ? 8 : 4);
     }
-    if ((multi || rp.in_end) && rs == 8) rs = 4;     // kOutAll / UNAL: 2- and 4-row strips
+    if ((multi || rp.in_end || rp.h16) && rs == 8) rs = 4;   // kOutAll / UNAL / H16: 2- and 4-row strips
     if (rp.in_end && knob(KN_UNAL_RS4)) rs = 4;
     rp.nstrips = (rows + rs - 1) / rs;
     const int64_t threads = rp.nstrips * rp.items;

@@ -52,6 +52,7 @@ enum Knob : int {
     KN_NO_FLAT,
     KN_K2P,
     KN_SYNC_BLOCK,
+    KN_NO_H16,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

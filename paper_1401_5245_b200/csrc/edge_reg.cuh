@@ -53,6 +53,7 @@ struct RegParams {
     int oswap;               // K2t2: 1 = uint64 output words (pixel word p at uint32 index p ^ 1)
     const char *in_end;      // K1 UNAL: end of the input buffer (loads stop there)
     int unal_words;          // K1 UNAL: load the 4 words one by one instead of 2 chunks
+    int h16;                 // K1: 8-word items from 16-byte (not 32-byte) aligned rows
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -113,6 +114,18 @@ __device__ __forceinline__ void store_chunk(uint32_t *p, const uint32_t (&v)[CW]
     }
 }
 
+// K1 item store: one CW-word vector store, or (H16: 16-byte aligned rows) two
+// 128-bit stores of an 8-word item.
+template <int CW, bool H16>
+__device__ __forceinline__ void store_item(uint32_t *p, const uint32_t (&v)[CW]) {
+    if constexpr (H16) {
+        __stcs(reinterpret_cast<uint4 *>(p), make_uint4(v[0], v[1], v[2], v[3]));
+        __stcs(reinterpret_cast<uint4 *>(p + 4), make_uint4(v[4], v[5], v[6], v[7]));
+    } else {
+        store_chunk<CW>(p, v);
+    }
+}
+
 // Item = CW pixel words of one row (memory order == pixel order for uint32 rows;
 // uint64 rows swap the halves of each word pair).  RS rows per strip.
 // PBM P4 rows (1 = black, MSB-first bytes).  A little-endian
@@ -166,9 +179,10 @@ inline bool k1_setup(const RegParams &p, K1Div &d) {
 // 8000 u32 4.95 vs 4.43 us, 8.6 vs 6.6 us serially); a row's last item may read
 // into the next row (padding positions) but never past `in_end`.  CW must be 4.
 template <int SWAP, int RS, int CW, int OUT, bool HALO, bool P4 = false, bool ALIGNED = false,
-          bool UNAL = false>
+          bool UNAL = false, bool H16 = false>
 __global__ void __launch_bounds__(kThreads, P4 ? (RS == 4 ? 3 : 4) : 0)   // P4: 3 (4-row) or 4 CTAs/SM; 0 = unset
 edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
+    static_assert(!H16 || (CW == 8 && !UNAL && !P4), "H16: 8-word items from 16-byte rows");
     pdl_wait();
     pdl_trigger();
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;   // < 2^32 (k1_setup)
@@ -217,6 +231,16 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
                 for (int q = 0; q < 4; ++q)
                     v[i][q] = ptr + 4 * q + 4 <= p.in_end ? __ldg((const uint32_t *)ptr + q) : 0u;
             }
+        } else if constexpr (H16) {
+            // rows that are 16-byte but not 32-byte multiples (the drop-in's uint64
+            // words at w % 128 in 65..127, e.g. 8000 px = 1008 B): 8-word items
+            // as two 128-bit loads, so the per-item work stays amortised over 8 words
+            // L1-allocating: a 32-byte sector holds lane L's second half and lane
+            // L+1's first (rows start at 16 mod 32), so the second request hits L1
+            const uint4 x = __ldg(reinterpret_cast<const uint4 *>(ptr));
+            const uint4 y = __ldg(reinterpret_cast<const uint4 *>(ptr + 16));
+            v[i][0] = x.x; v[i][1] = x.y; v[i][2] = x.z; v[i][3] = x.w;
+            v[i][4] = y.x; v[i][5] = y.y; v[i][6] = y.z; v[i][7] = y.w;
         } else {
             load_chunk<CW>(ptr, v[i]);               // P4: raw bytes, converted per use
         }
@@ -293,7 +317,7 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
                                      : which == 3 ? x.r : which == 4 ? x.u : which == 5 ? x.d : x.pk;
                     }
                     if (nst == CW && p.vst) {
-                        store_chunk<CW>(dst + o, tw);
+                        store_item<CW, H16>(dst + o, tw);
                     } else {
                         for (int q = 0; q < nst; ++q) dst[o + q] = tw[q];
                     }
@@ -324,8 +348,8 @@ edge_reg_packed_kernel(const RegParams p, const K1Div dv) {
 #pragma unroll
                 for (int q = 0; q < CW; ++q) word(q);
                 if (nst == CW && p.vst) {
-                    if (OUT != kOutEset) store_chunk<CW>(p.o_edges + o, ve);
-                    if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + o, vs);
+                    if (OUT != kOutEset) store_item<CW, H16>(p.o_edges + o, ve);
+                    if (OUT != kOutEdges) store_item<CW, H16>(p.o_eset + o, vs);
                 } else {
                     for (int q = 0; q < nst; ++q) {
                         if (OUT != kOutEset) p.o_edges[o + q] = ve[q];

@@ -1,0 +1,20 @@
+# Round 2 refresh in one call: smoke, the whole GPU suite, every config's bench line
+# (20 steps, as the driver runs them; the default line = C4) and the reference arm,
+# widths + drop-in tables, then the profiling pass (launch list of the default bench,
+# one full ncu capture per config).  Results: gpurun_out/fin/ and gpurun_out/prof/.
+set -u
+mkdir -p gpurun_out/fin
+leftovers() { nvidia-smi --query-compute-apps=pid --format=csv,noheader 2>/dev/null | while read p; do [ -n "$p" ] && kill -9 "$p" 2>/dev/null && echo "killed leftover $p"; done; }
+timeout -k 10 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/fin/smoke.log
+timeout -k 10 1500 python -m pytest tests -q -m gpu -p no:cacheprovider -rf > gpurun_out/fin/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/fin/pytest.log; leftovers >> gpurun_out/fin/pytest.log
+timeout -k 10 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/fin/bench_c4.json 2> gpurun_out/fin/bench_c4.err
+timeout -k 10 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/fin/ref_c4.json 2> gpurun_out/fin/ref_c4.err
+for c in c1 c2 c3 c5; do
+  timeout -k 10 900 python bench.py --config $c --gpus 1 --steps 20 --warmup 5 > gpurun_out/fin/bench_$c.json 2> gpurun_out/fin/bench_$c.err
+done
+timeout -k 10 300 python scripts/k1_widths.py > gpurun_out/fin/k1w.log 2>&1
+timeout -k 10 300 python scripts/u8_widths.py > gpurun_out/fin/u8w.log 2>&1
+timeout -k 10 300 python scripts/dropin_latency.py gpurun_out/fin/dropin.json > gpurun_out/fin/dropin.log 2>&1
+timeout -k 10 600 python scripts/bench_next.py gpurun_out/fin/bench_next.json > gpurun_out/fin/bench_next.log 2>&1
+TAG=r2 LAUNCH_CFG=c4 timeout -k 10 1800 bash scripts/gpu_profiles.sh > gpurun_out/fin/profiles.log 2>&1
+echo done

@@ -8,6 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1401_5245_b200 import _capi  # noqa: E402
 from paper_1401_5245_b200 import pbm  # noqa: E402
 
 dev = torch.device("cuda:0")
@@ -23,6 +24,7 @@ for (h, w) in ((8000, 8000), (8000, 7993), (2000, 2000), (256, 250)):
             os.environ["BITEDGE_P4_UNFUSED"] = "1"
         else:
             os.environ.pop("BITEDGE_P4_UNFUSED", None)
+        _capi.reload_knobs()                       # knobs are read once per process
         for i in range(3):
             pbm.detect_p4(ins[i % pool], 1, h, w, out=outs[i % pool])
         torch.cuda.synchronize()

@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out", "prof")
 DST = os.environ.get("PROF_DST", os.path.join(ROOT, "profiles"))
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
+LCFG = os.environ.get("LAUNCH_CFG", "c2")         # the bench config of the launch list
 ALG = {"c1": 256 * 256 * 1.125, "c2": 4096 * 64 * 64 * 1.125, "c3": 8192 * 8192 * 0.25,
        "c4": 65536 * 65536 * 0.25, "c5": 1024 * 2048 * 2048 * 1.125}
 WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput",
@@ -30,7 +31,7 @@ def ncu_csv(rep, page, extra=()):
 
 
 def launch_list():
-    path = os.path.join(SRC, "launches_bench_c2.csv")
+    path = os.path.join(SRC, f"launches_bench_{LCFG}.csv")
     rows = list(csv.reader(open(path)))
     hdr = None
     per = collections.OrderedDict()
@@ -42,7 +43,7 @@ def launch_list():
             d = dict(zip(hdr, r))
             k = (d["ID"], d["Kernel Name"])
             per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
-    out = os.path.join(DST, f"{TAG}_launches_bench_c2.csv")
+    out = os.path.join(DST, f"{TAG}_launches_bench_{LCFG}.csv")
     share = collections.Counter()
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
@@ -115,7 +116,7 @@ def main():
              "~0 per launch: the write-back L2 (126 MB) still holds them when the replay's",
              "counters stop, and they reach DRAM only on eviction; the bench's rotating",
              "buffer pools (> 3x L2) make every step pay that write-back eventually.", "",
-             f"## Launch list of `python bench.py --config c2 --steps 200 --warmup 5 --no-cpu` ({nl} launches)",
+             f"## Launch list of `{os.environ.get('LAUNCH_CMD', 'python bench.py --config ' + LCFG)}` ({nl} launches)",
              "", "| kernel | share of GPU time |", "|---|---|"]
     lines += [f"| `{k}` | {v:.1%} |" for k, v in shares]
     lines += ["", "## Top kernel per config (one launch, full section set)", ""]

@@ -42,6 +42,7 @@ VARIANTS = {
     "unal_bytes": {"BITEDGE_UNAL_BYTES": "1"},
     "u64_tma": {"BITEDGE_U64_TMA": "1"},
     "k2p": {"BITEDGE_K2P": "1"},
+    "no_h16": {"BITEDGE_NO_H16": "1"},
     "no_flat": {"BITEDGE_NO_FLAT": "1"},
 }
 
