@@ -54,13 +54,13 @@ def test_hot_kernel_register_budget(frag, budget):
 # cache misses (676 -> 994 us) with no change in registers.
 SASS_BUDGET = {
     # K1, tail-free (w % 256 == 0) variants: C3, C4, C4 row slabs, P4 (F1)
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb1ELb0EEEvNS_9RegParamsENS_5K1DivE": 500,
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb1ELb0EEEvNS_9RegParamsENS_5K1DivE": 800,
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb1ELb0ELb1ELb0EEEvNS_9RegParamsENS_5K1DivE": 800,
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb1ELb1ELb0EEEvNS_9RegParamsENS_5K1DivE": 850,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb1ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 500,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb1ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 800,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb1ELb0ELb1ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 800,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb1ELb1ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 850,
     # K1 general (ragged widths)
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 950,
-    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 1450,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 950,
+    "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 1450,
     "_ZN7bitedge20edge_warp_img_kernelILi1ELi0ELi8EEEvNS_9RegParamsEil": 1550,
     "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0EEEvNS_9RegParamsEll": 2800,
 }
