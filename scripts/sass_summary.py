@@ -32,10 +32,12 @@ CLASSES = [
 ]
 HOT = [  # (label, substring of the demangled name)
     ("K1 aligned, 2-row strips (C3 packed u32)",
-     "edge_reg_packed_kernel<0, 2, 8, 0, false, false, true, false>"),
+     "edge_reg_packed_kernel<0, 2, 8, 0, false, false, true, false, false>"),
     ("K1 aligned, 4-row strips (C4 packed u32, the headline)",
-     "edge_reg_packed_kernel<0, 4, 8, 0, false, false, true, false>"),
-    ("K3 halo (C4 row shards)", "edge_reg_packed_kernel<0, 4, 8, 0, true, false, true, false>"),
+     "edge_reg_packed_kernel<0, 4, 8, 0, false, false, true, false, false>"),
+    ("K3 halo (C4 row shards)", "edge_reg_packed_kernel<0, 4, 8, 0, true, false, true, false, false>"),
+    ("K3e end rows of a row shard", "edge_halo_ends_kernel"),
+    ("K1 H16 (16-byte rows, 8-word items)", "edge_reg_packed_kernel<0, 2, 8, 0, false, false, false, false, true>"),
     ("K1f flat (ragged packed rows)", "edge_flat_kernel<8, 0, 6, 0>"),
     ("K2w warp-per-image (C2 glyphs)", "edge_warp_img_kernel<1, 0, 8>"),
     ("K2t2 TMA ring (C5 pages)", "edge_tma2_u8_kernel<8, 4, 0, false>"),
