@@ -259,6 +259,74 @@ int launch_flat_cw(const FlatParams &fp, int ru, unsigned grid, cudaStream_t st)
     return kNoKernel;
 }
 
+// K1s (edge_flat.cuh): contiguous ragged packed rows staged through a per-warp
+// shared-memory ring.  LR = log2(ring words per warp): 2^11 (8 KB, 3 CTAs/SM)
+// while one step's window of pieces leaves >= 2 slots for prefetch, else 2^12.
+template <int SWAP, int OUT, int LR>
+int launch_flat_ring(const FlatRingParams &fr, unsigned grid, size_t smem, cudaStream_t st) {
+    auto kern = edge_flat_ring_kernel<SWAP, OUT, LR>;
+    static bool attr = false;                         // (per instantiation)
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    launch_k(kern, grid, smem, st, fr);
+    return cuda_check("edge_flat_ring_kernel");
+}
+
+int try_flat_ring(const void *in, uint32_t *o_edges, uint32_t *o_eset, const Geometry &G,
+                  int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
+    // opt-in (BITEDGE_RING): as fast as K1f on large ragged rasters (both at the
+    // copy peak), slower on small ones (per-warp ring start-up)
+    if (!knob(KN_RING) || knob(KN_NO_FLAT)) return kNoKernel;
+    const int64_t S = G.wp;
+    const int64_t nwords = nrows * S;
+    if (row_lo != 0 || row_hi != nrows || nwords >= ((int64_t)1 << 31) - 4096 || S < 64 ||
+        nwords % 4 != 0 || G.h >= ((int64_t)1 << 31))
+        return kNoKernel;
+    auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+    if (!al(in, 16) || !al(o_edges, 8) || !al(o_eset, 8)) return kNoKernel;
+    // pieces one 256-word step reads: <= ceil((2S + 259) / 256) + 1; keep >= 2
+    // slots for prefetch
+    const int64_t window = (2 * S + 259 + kRingSegW - 1) / kRingSegW + 1;
+    int lr;
+    if (window + 2 <= (1 << 11) / kRingSegW) lr = 11;
+    else if (window + 2 <= (1 << 12) / kRingSegW) lr = 12;
+    else return kNoKernel;
+    const int warps_per_sm = lr == 11 ? 24 : 8;       // smem: 3 / 1 CTAs of 8 warps per SM
+    const int64_t maxw = (int64_t)sm_count() * warps_per_sm;
+    int64_t minspan = 4 * S > 1024 ? 4 * S : 1024;    // halo reads <= 2S per span
+    int64_t nwarps = (nwords + minspan - 1) / minspan;
+    if (nwarps > maxw) nwarps = maxw;
+    if (nwarps < 1) nwarps = 1;
+    int64_t span = (nwords + nwarps - 1) / nwarps;
+    span = (span + 255) / 256 * 256;
+    nwarps = (nwords + span - 1) / span;
+    FlatRingParams fr;
+    memset(&fr, 0, sizeof(fr));
+    fr.in = (const uint32_t *)in;
+    fr.o_edges = o_edges; fr.o_eset = o_eset;
+    fr.nwords = (uint32_t)nwords; fr.S = (uint32_t)S; fr.h = (uint32_t)G.h;
+    fr.pl = G.pl; fr.lastbit = G.lastbit; fr.padmask = G.padmask; fr.fillword = G.fillword;
+    fr.span = (uint32_t)span; fr.nwarps = (uint32_t)nwarps;
+    fr.div_s = make_fastdiv((uint32_t)S);
+    fr.div_h = make_fastdiv((uint32_t)G.h);
+    const int rw = 1 << lr;
+    const size_t smem = (size_t)8 * rw * 4 + (size_t)8 * (rw / kRingSegW) * 8;
+    const unsigned grid = (unsigned)((nwarps + 7) / 8);
+    const int out = (o_edges && o_eset) ? kOutAny : o_eset ? kOutEset : kOutEdges;
+#define BE_RING(SW, LRV)                                                                  \
+    return out == kOutAny ? launch_flat_ring<SW, kOutAny, LRV>(fr, grid, smem, st)        \
+         : out == kOutEset ? launch_flat_ring<SW, kOutEset, LRV>(fr, grid, smem, st)      \
+                           : launch_flat_ring<SW, kOutEdges, LRV>(fr, grid, smem, st);
+    if (G.swap) {
+        if (lr == 11) { BE_RING(1, 11) } else { BE_RING(1, 12) }
+    } else {
+        if (lr == 11) { BE_RING(0, 11) } else { BE_RING(0, 12) }
+    }
+#undef BE_RING
+}
+
 int try_flat(const void *in, uint32_t *o_edges, uint32_t *o_eset, const Geometry &G,
              int64_t nrows, int64_t row_lo, int64_t row_hi, cudaStream_t st) {
     if (knob(KN_NO_FLAT)) return kNoKernel;
@@ -362,7 +430,9 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         // contiguous rows (stride == row length): the flat kernel's aligned vector
         // accesses instead of K1's word-by-word items
         if (in_row_bytes == (int64_t)G.wp * 4 && out_stride_u32 == G.wp) {
-            const int rc = try_flat(in, o_edges, o_eset, G, nrows, row_lo, row_hi, st);
+            int rc = try_flat_ring(in, o_edges, o_eset, G, nrows, row_lo, row_hi, st);
+            if (rc != kNoKernel) return rc;
+            rc = try_flat(in, o_edges, o_eset, G, nrows, row_lo, row_hi, st);
             if (rc != kNoKernel) return rc;
         }
         rp.in_end = (const char *)in + (nrows - 1) * in_row_bytes + (int64_t)G.wp * 4;

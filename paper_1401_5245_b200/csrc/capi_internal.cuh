@@ -53,6 +53,7 @@ enum Knob : int {
     KN_K2P,
     KN_SYNC_BLOCK,
     KN_NO_H16,
+    KN_RING,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

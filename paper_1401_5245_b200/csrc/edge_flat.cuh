@@ -199,4 +199,167 @@ edge_flat_kernel(const FlatParams p) {
     }
 }
 
+// ---------------------------------------------------------------- K1s
+// The same flat view, staged through a per-warp ring in shared memory so each
+// input word crosses L2 about once (K1f reads the rows above and below every
+// chunk again: 3x L2 reads, L2-throughput-bound).
+//
+// Warp g owns the output words [g * span, (g + 1) * span) of the flat array and
+// streams the input words [start - S - 2, end + S + 2) (16-byte aligned) through
+// a circular buffer of RW = 2^LR words indexed by flat word index mod RW, in
+// pieces cut at multiples of SEGW words: piece k lands in slot k mod NSLOT with
+// one `cp.async.bulk` (lane 0) and its own mbarrier.  Each step the warp
+// produces 256 output words (4 pairs per lane, 64-bit stores) from the ring: the
+// centre pair, the pairs S words before / after it and the two neighbour words
+// are shared-memory loads at any word offset; the row structure per word is as
+// in K1f.  Before a step, the pieces it reads are waited for; then every piece
+// whose slot's previous piece no later step reads is issued, so up to
+// NSLOT - (pieces one step reads) pieces are in flight per warp.
+struct FlatRingParams {
+    const uint32_t *in;      // 16-byte aligned
+    uint32_t *o_edges;       // 8-byte aligned (or nullptr)
+    uint32_t *o_eset;
+    uint32_t nwords;         // nrows * S, a multiple of 4, < 2^31
+    uint32_t S, h;
+    int pl;
+    uint32_t lastbit, padmask, fillword;
+    uint32_t span;           // output words per warp, a multiple of 256
+    uint32_t nwarps;
+    FastDiv div_s, div_h;
+};
+
+constexpr int kRingSegW = 256;                        // words per piece / slot
+
+template <int SWAP, int OUT, int LR>
+__global__ void __launch_bounds__(kThreads)
+edge_flat_ring_kernel(const FlatRingParams p) {
+    constexpr int RW = 1 << LR, MASK = RW - 1;
+    constexpr int NSLOT = RW / kRingSegW;
+    constexpr int WARPS = kThreads / 32;
+    extern __shared__ __align__(128) uint32_t k1s_smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *ring = k1s_smem + (size_t)wid * RW;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(k1s_smem + (size_t)WARPS * RW) + wid * NSLOT;
+    if (lane == 0) {
+        for (int i = 0; i < NSLOT; ++i) wbar_init(&bars[i]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t gw = blockIdx.x * WARPS + wid;
+    if (gw >= p.nwarps) return;                       // whole warp, no CTA barriers
+    const int64_t S = p.S, nw = p.nwords;
+    const int64_t o0 = (int64_t)gw * p.span;
+    if (o0 >= nw) return;
+    const int64_t o1 = o0 + p.span < nw ? o0 + p.span : nw;
+    // input words this warp stages (16-byte granules; the buffer ends clamp)
+    int64_t i0 = o0 - S - 2;
+    i0 = i0 < 0 ? 0 : (i0 & ~(int64_t)3);
+    int64_t i1 = (o1 + S + 2 + 3) & ~(int64_t)3;
+    i1 = i1 > nw ? nw : i1;
+    const int64_t k0 = i0 / kRingSegW, klast = (i1 - 1) / kRingSegW;
+    int64_t issued = k0, ready = k0;                  // next piece to issue / to wait for
+    auto issue_upto = [&](int64_t kend) {             // lane 0: pieces [issued, kend]
+        if (kend > klast) kend = klast;
+        if (issued <= kend) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (; issued <= kend; ++issued) {
+            const int64_t a = issued * kRingSegW > i0 ? issued * kRingSegW : i0;
+            const int64_t b = (issued + 1) * kRingSegW < i1 ? (issued + 1) * kRingSegW : i1;
+            uint64_t *bar = &bars[issued % NSLOT];
+            wbar_expect(bar, (uint32_t)(b - a) * 4u);
+            wtma(ring + (a & MASK), p.in + a, (uint32_t)(b - a) * 4u, bar);
+        }
+    };
+    if (lane == 0) issue_upto(k0 + NSLOT - 1);
+
+    const uint32_t fw = p.fillword;
+    const uint32_t h = p.h;
+    const uint32_t S32 = p.S;
+    // a step = 256 output words = 4 pairs per lane (pair q of lane l: words
+    // f0 + 64q + 2l, +1 -- every shared-memory load of the warp is contiguous)
+    for (int64_t f0 = o0; f0 < o1; f0 += 256) {
+        int64_t need = (f0 + 255 + S + 2) / kRingSegW;
+        need = need > klast ? klast : need;
+        for (; ready <= need; ++ready)
+            wbar_wait(&bars[ready % NSLOT], (uint32_t)(((ready - k0) / NSLOT) & 1));
+        uint32_t c[4][2], u[4][2], d[4][2], lw[4], rw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t f = f0 + 64 * q + 2 * lane;
+            const uint2 m = *reinterpret_cast<const uint2 *>(ring + (f & MASK));
+            c[q][0] = SWAP ? m.y : m.x;
+            c[q][1] = SWAP ? m.x : m.y;
+            uint32_t a0, a1, b0, b1;
+            if ((S & 1) == 0) {                       // pairs stay 8-byte aligned
+                const uint2 mu = *reinterpret_cast<const uint2 *>(ring + ((f - S) & MASK));
+                const uint2 md = *reinterpret_cast<const uint2 *>(ring + ((f + S) & MASK));
+                a0 = mu.x; a1 = mu.y; b0 = md.x; b1 = md.y;
+            } else {
+                a0 = ring[(f - S) & MASK]; a1 = ring[(f - S + 1) & MASK];
+                b0 = ring[(f + S) & MASK]; b1 = ring[(f + S + 1) & MASK];
+            }
+            u[q][0] = SWAP ? a1 : a0; u[q][1] = SWAP ? a0 : a1;
+            d[q][0] = SWAP ? b1 : b0; d[q][1] = SWAP ? b0 : b1;
+            lw[q] = ring[(f - 1 - SWAP) & MASK];      // pixel word f - 1
+            rw[q] = ring[(f + 2 + SWAP) & MASK];      // pixel word f + 2
+        }
+        // every lane has read this step's words: slots behind the next step's
+        // lowest word are free
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t lo_next = f0 + 256 - S - 2;
+            const int64_t kmin = lo_next <= i0 ? k0 : lo_next / kRingSegW;
+            issue_upto(kmin + NSLOT - 1);
+        }
+        // row / column of the first pair; +64 words per pair (S >= 64: one wrap)
+        const uint32_t fa = (uint32_t)(f0 + 2 * lane);
+        const uint32_t r0 = fdiv(fa, p.div_s);
+        uint32_t col = fa - r0 * S32;
+        uint32_t y = r0 - fdiv(r0, p.div_h) * h;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t f = f0 + 64 * q + 2 * lane;
+            if (q > 0) {
+                col += 64;
+                if (col >= S32) {
+                    col -= S32;
+                    y = y + 1 == h ? 0 : y + 1;
+                }
+            }
+            uint32_t ve[2], vs[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                uint32_t cj = col + j, yj = y;
+                if (j == 1 && cj == S32) {            // u32 rows of odd length: f + 1 wraps
+                    cj = 0;
+                    yj = y + 1 == h ? 0 : y + 1;
+                }
+                const uint32_t left = j == 0 ? lw[q] : c[q][0];
+                const uint32_t right = j == 1 ? rw[q] : c[q][1];
+                const uint32_t ln = __funnelshift_r(c[q][j], cj == 0 ? fw : left, 1);
+                uint32_t rn = __funnelshift_l(right, c[q][j], 1);
+                const uint32_t uu = yj == 0 ? fw : u[q][j];
+                const uint32_t dd = yj == h - 1 ? fw : d[q][j];
+                uint32_t force = 0u;
+                if ((int)cj == p.pl) {
+                    rn = (rn & ~p.lastbit) | (fw & p.lastbit);
+                    force = p.padmask;
+                } else if ((int)cj > p.pl) {
+                    force = 0xFFFFFFFFu;
+                }
+                const uint32_t any = ln | rn | uu | dd;
+                ve[j ^ SWAP] = c[q][j] | ~any | force;
+                vs[j ^ SWAP] = (~c[q][j] & any) | force;
+            }
+            if (f < o1) {
+                if (OUT != kOutEset)
+                    __stcs(reinterpret_cast<uint2 *>(p.o_edges + f), make_uint2(ve[0], ve[1]));
+                if (OUT != kOutEdges)
+                    __stcs(reinterpret_cast<uint2 *>(p.o_eset + f), make_uint2(vs[0], vs[1]));
+            }
+        }
+    }
+}
+
 }  // namespace bitedge

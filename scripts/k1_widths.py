@@ -35,7 +35,7 @@ def timed(step, k, nstreams):
 
 for bits in (32, 64):
     for (h, w) in ((8192, 8192), (8192, 8000), (8192, 8064), (8192, 8160), (8192, 7999),
-                   (4096, 16384 - 32)):
+                   (4096, 16384 - 32), (32768, 32000)):
         wp = -(-w // bits)
         dt = torch.int32 if bits == 32 else torch.int64
         nbytes = h * wp * bits // 8

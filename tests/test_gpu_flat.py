@@ -1,5 +1,7 @@
-"""K1f (edge_flat.cuh): packed rows whose length is not a multiple of the vector
-width, viewed as one flat word array -- bit-exact against the per-pixel C
+"""K1f / K1s (edge_flat.cuh): packed rows whose length is not a multiple of the
+vector width, viewed as one flat word array (K1f register-direct, the default;
+K1s staged through a per-warp shared-memory ring, opt-in) -- bit-exact against
+the per-pixel C
 oracle (u32 rows) and the reference composition (the drop-in's uint64 words),
 for every realignment phase, 32- and 16-byte buffer alignment, batches, both
 border policies and both outputs; and identical to the K1 UNAL kernel it
@@ -26,16 +28,24 @@ def _aligned_view(torch, n_words, dtype, dev, offset_words):
 U32_WIDTHS = [8000, 7999, 8160, 4100, 520, 600, 1056, 513, 700, 640, 660, 16 * 32 * 3 + 5]
 
 
+@pytest.fixture(params=["flat", "ring"])
+def flat_kernel(request, monkeypatch):
+    """K1f (default) or K1s (opt-in, BITEDGE_RING, where it applies)."""
+    if request.param == "ring":
+        monkeypatch.setenv("BITEDGE_RING", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("w", U32_WIDTHS)
 @pytest.mark.parametrize("offset", [0, 4], ids=["a32", "a16"])
-def test_flat_u32(cuda_dev, w, offset):
+def test_flat_u32(cuda_dev, w, offset, flat_kernel):
     import torch
 
     from paper_1401_5245_b200 import cuda as cu
 
     rng = np.random.default_rng(w * 7 + offset)
     wp = -(-w // 32)
-    for n, h in ((1, 1), (1, 2), (1, 37), (3, 5), (2, 64)):
+    for n, h in ((1, 1), (1, 2), (1, 37), (3, 5), (2, 64), (4, 33), (1, 1000), (5, 200)):
         words = rng.integers(0, 2**32, (n, h, wp), dtype=np.uint32)
         src = _aligned_view(torch, n * h * wp, torch.int32, cuda_dev, offset).view(n, h, wp)
         src.copy_(torch.from_numpy(words.view(np.int32)))
@@ -52,14 +62,14 @@ def test_flat_u32(cuda_dev, w, offset):
 
 @pytest.mark.parametrize("w", [8000, 1100, 8100, 1300, 2600, 4100])
 @pytest.mark.parametrize("offset", [0, 4], ids=["a32", "a16"])
-def test_flat_u64_dropin_words(cuda_dev, w, offset):
+def test_flat_u64_dropin_words(cuda_dev, w, offset, flat_kernel):
     import torch
 
     from paper_1401_5245_b200 import cuda as cu
 
     rng = np.random.default_rng(w + offset)
     wp64 = -(-w // 64)
-    for h in (1, 3, 40):
+    for h in (1, 3, 40, 1000):
         a = (rng.random((h, w)) < 0.5).astype(np.uint8)
         ref = P.from_array(a)
         src = _aligned_view(torch, h * wp64 * 2, torch.int64, cuda_dev, offset).view(h, wp64)

@@ -43,6 +43,7 @@ VARIANTS = {
     "u64_tma": {"BITEDGE_U64_TMA": "1"},
     "k2p": {"BITEDGE_K2P": "1"},
     "no_h16": {"BITEDGE_NO_H16": "1"},
+    "ring": {"BITEDGE_RING": "1"},
     "no_flat": {"BITEDGE_NO_FLAT": "1"},
 }
 
