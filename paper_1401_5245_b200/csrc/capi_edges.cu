@@ -184,17 +184,19 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 
 // K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA).
-template <int RSL>
+template <int RSL, bool UNAL = false>
 int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t st) {
     constexpr int kD = 4;
     const int64_t nstrips = (rows_total(rp.row_lo, rp.row_hi) + RSL - 1) / RSL;
     const int64_t nwarps = nstrips * nseg;
     const unsigned grid = (unsigned)((nwarps + 7) / 8);
-    const size_t smem = (size_t)8 * kD * 2080 + (size_t)8 * kD * 8;
+    // ring slot: 16 + 2048 + 16 bytes (+32 for UNAL: granule-aligned copies)
+    const size_t smem = (size_t)8 * kD * (UNAL ? 2112 : 2080) + (size_t)8 * kD * 8;
     rp.nstrips = nstrips;
+    if (UNAL && halo) return kNoKernel;
 #define BE_TMA2(OUTK, H)                                                                        \
     do {                                                                                        \
-        auto kern = edge_tma2_u8_kernel<RSL, kD, OUTK, H>;                                      \
+        auto kern = edge_tma2_u8_kernel<RSL, kD, OUTK, H && !UNAL, UNAL>;                      \
         /* per launch: the attribute is per device, and these launches are long */             \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         launch_k(kern, grid, smem, st, rp, nseg, nwarps);                                       \
@@ -230,6 +232,20 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
     rp.items = G.wp;
     rp.thr = thr;
+    // rows >= 2048 px with enough work: the TMA ring (K2t2) with granule-aligned
+    // copies and a per-row realignment of the packed words (16384 x 16100: 0.45 ->
+    // see DESIGN.md section 4); K2 UNAL below otherwise
+    if (G.w >= 2048 && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
+        const int64_t nseg = (G.w + 2047) / 2048;
+        const int64_t nwarps32 = (row_hi - row_lo + 31) / 32 * nseg;
+        const bool force = knob(KN_FORCE_TMA) != nullptr;
+        if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
+            const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) && !knob(KN_TMA2_RSL32);
+            const bool multi = o_packed != nullptr;
+            return short_strips ? launch_tma2<8, true>(rp, multi, false, nseg, st)
+                                : launch_tma2<32, true>(rp, multi, false, nseg, st);
+        }
+    }
     {   // alignment of every row start (base and row stride)
         const uintptr_t a = (uintptr_t)in | (uintptr_t)in_row_bytes;
         rp.v8 = (a % 8 == 0 && !knob(KN_UNAL_BYTES)) ? 8

@@ -54,6 +54,7 @@ enum Knob : int {
     KN_SYNC_BLOCK,
     KN_NO_H16,
     KN_RING,
+    KN_NO_TMA_UNAL,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

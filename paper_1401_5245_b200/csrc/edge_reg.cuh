@@ -1010,12 +1010,20 @@ edge_tma_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
 // at ~200 instructions per 1 KB row segment.  Staged rows are addressed with
 // integer offsets from one base pointer; only the first/last staged rows can be
 // absent or come from the halo buffers.
-template <int RSL, int D, int OUT, bool HALO>
+// UNAL: uint8 rows at any byte offset (row lengths that are not 16-byte
+// multiples).  A staged row segment starts at the 16-byte granule holding its
+// first byte, delta = (address & 15) bytes early, so lane L's aligned 32 bytes
+// are pixels x0 + 32L - delta ..; each lane packs them as for aligned rows and
+// shifts the packed word left by delta bits, taking the low bits from the next
+// lane's packed word (one shuffle + one funnel shift per word; lane 31 packs 16
+// more bytes).  Every copy stays inside the granules of valid row bytes.
+template <int RSL, int D, int OUT, bool HALO, bool UNAL = false>
 __global__ void __launch_bounds__(kThreads, 3)   // smem allows 3 CTAs/SM: up to 80 regs, no spills
 edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
+    static_assert(!(UNAL && HALO), "UNAL: no halo rows");
     const Thr T = make_thr(p.thr);
     constexpr int SEG = 2048;                        // pixels (bytes) per warp segment
-    constexpr int SLOT = 16 + SEG + 16;
+    constexpr int SLOT = UNAL ? 16 + SEG + 48 : 16 + SEG + 16;
     constexpr int WARPS = kThreads / 32;
     extern __shared__ __align__(128) char tsm[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1066,8 +1074,17 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
         if (top_halo && i == 0) src = p.above + b_lo;
         if (bot_halo && i == i_hi) src = p.below + b_lo;
         uint64_t *b = &bars[k % D];
-        wbar_expect(b, seg_bytes);
-        wtma(ring + (k % D) * SLOT + dst_off, src, seg_bytes, b);
+        if constexpr (UNAL) {
+            // [granule of the first byte, end of the granule of the last byte)
+            const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+            const int64_t end_px = x0 + SEG + 16 < p.w ? x0 + SEG + 16 : p.w;
+            const uintptr_t a1 = ((uintptr_t)(src - b_lo + end_px) + 15) & ~(uintptr_t)15;
+            wbar_expect(b, (uint32_t)(a1 - a0));
+            wtma(ring + (k % D) * SLOT + dst_off, (const char *)a0, (uint32_t)(a1 - a0), b);
+        } else {
+            wbar_expect(b, seg_bytes);
+            wtma(ring + (k % D) * SLOT + dst_off, src, seg_bytes, b);
+        }
     };
     if (lane == 0)
         for (int k = 0; k < D; ++k) issue(k);
@@ -1096,8 +1113,22 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
                            *reinterpret_cast<const uint4 *>(s + 32 * lane + 16), T);
             b = pack32_any(*reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane),
                            *reinterpret_cast<const uint4 *>(s + 1024 + 32 * lane + 16), T);
-            if (lane == 0) el = (uint8_t)s[-1] >= T.t ? 1u : 0u;
-            if (lane == 31) er = (uint8_t)s[SEG] >= T.t ? 0x80000000u : 0u;
+            int dl = 0;
+            if constexpr (UNAL) {
+                dl = (int)((uintptr_t)(base + i * rb) & 15);        // warp-uniform
+                uint32_t xb_ = 0u;                                // lane 31: bytes 2048 .. 2063
+                if (lane == 31)
+                    xb_ = pack32_any(*reinterpret_cast<const uint4 *>(s + SEG),
+                                     make_uint4(0u, 0u, 0u, 0u), T);
+                const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, b, 0);
+                uint32_t na = __shfl_down_sync(0xFFFFFFFFu, a, 1);
+                uint32_t nb = __shfl_down_sync(0xFFFFFFFFu, b, 1);
+                if (lane == 31) { na = b0; nb = xb_; }
+                a = __funnelshift_l(na, a, dl);
+                b = __funnelshift_l(nb, b, dl);
+            }
+            if (lane == 0) el = (uint8_t)s[dl - 1] >= T.t ? 1u : 0u;
+            if (lane == 31) er = (uint8_t)s[dl + SEG] >= T.t ? 0x80000000u : 0u;
         }
         __syncwarp();
         if (lane == 0) issue(k + D);                 // slot free (consumed or unused)

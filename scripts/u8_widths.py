@@ -34,7 +34,7 @@ def timed(step, k, nstreams):
     return a.elapsed_time(b) * 1e3 / k
 
 
-for (n, h, w) in ((1, 4096, 4096), (1, 4096, 4100), (1, 4096, 4000), (16, 1024, 1024), (16, 1024, 1000),
+for (n, h, w) in ((1, 16384, 16384), (1, 16384, 16100), (1, 16384, 16001), (1, 4096, 4096), (1, 4096, 4100), (1, 4096, 4000), (16, 1024, 1024), (16, 1024, 1000),
                   (64, 256, 256), (64, 256, 250)):
     nbytes = n * h * w
     pool = max(2, min(48, (3 * 126 << 20) // nbytes + 1))

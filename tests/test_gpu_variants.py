@@ -50,7 +50,7 @@ VARIANTS = {
 # (n, h, w): glyph batches, wide pages, ragged widths, single rows / columns
 SHAPES = [(64, 64, 64), (8, 32, 32), (3, 40, 2048), (2, 70, 4160), (5, 33, 100), (1, 1, 1), (3, 50, 8000), (2, 9, 1000),
           (1, 300, 1), (1, 1, 700), (4, 16, 256), (2, 200, 8192), (1500, 32, 32),
-          (600, 16, 64), (333, 64, 128)]
+          (600, 16, 64), (333, 64, 128), (2, 37, 4100), (1, 19, 2050), (3, 21, 6001)]
 
 
 def _t(a, dev):

@@ -62,7 +62,8 @@ SASS_BUDGET = {
     "_ZN7bitedge22edge_reg_packed_kernelILi0ELi2ELi8ELi0ELb0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 950,
     "_ZN7bitedge22edge_reg_packed_kernelILi0ELi4ELi8ELi0ELb0ELb0ELb0ELb0ELb0EEEvNS_9RegParamsENS_5K1DivE": 1450,
     "_ZN7bitedge20edge_warp_img_kernelILi1ELi0ELi8EEEvNS_9RegParamsEil": 1550,
-    "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0EEEvNS_9RegParamsEll": 2800,
+    "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0ELb0EEEvNS_9RegParamsEll": 2800,
+    "_ZN7bitedge19edge_tma2_u8_kernelILi8ELi4ELi0ELb0ELb1EEEvNS_9RegParamsEll": 3300,   # UNAL rows
 }
 
 
