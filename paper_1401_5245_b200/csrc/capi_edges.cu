@@ -139,10 +139,17 @@ int launch_reg_u8(RegParams &rp, int rs, unsigned grid, cudaStream_t st) {
         if constexpr (HALO) {
             return kNoKernel;
         } else {
-            // widest alignment every row start has (rp.v8 carries it: 8, 4 or 1)
-            if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, 0, st, rp);
-            else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, 0, st, rp);
-            else launch_k(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, 0, st, rp);
+            // widest alignment every row start has (rp.v8 carries it: 8, 4 or 1);
+            // 2-row strips for small rasters (twice the threads in flight)
+            if (rs == 2) {
+                if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<2, OUT, false, false, 8>, grid, 0, st, rp);
+                else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<2, OUT, false, false, 4>, grid, 0, st, rp);
+                else launch_k(edge_reg_u8_kernel<2, OUT, false, false, 1>, grid, 0, st, rp);
+            } else {
+                if (rp.v8 == 8) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 8>, grid, 0, st, rp);
+                else if (rp.v8 == 4) launch_k(edge_reg_u8_kernel<4, OUT, false, false, 4>, grid, 0, st, rp);
+                else launch_k(edge_reg_u8_kernel<4, OUT, false, false, 1>, grid, 0, st, rp);
+            }
             return cuda_check("edge_reg_u8_kernel<UNAL>");
         }
     }
@@ -232,14 +239,15 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     rp.lastbit = G.lastbit; rp.padmask = G.padmask; rp.fillword = G.fillword;
     rp.items = G.wp;
     rp.thr = thr;
-    // rows >= 2048 px with enough work: the TMA ring (K2t2) with granule-aligned
-    // copies and a per-row realignment of the packed words (16384 x 16100: 0.45 ->
-    // see DESIGN.md section 4); K2 UNAL below otherwise
+    // rows >= 2048 px: the TMA ring (K2t2) with granule-aligned copies and a
+    // per-row realignment of the packed words (16384 x 16100: 45 -> 95 % of the
+    // copy peak); K2 UNAL below otherwise
     if (G.w >= 2048 && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (row_hi - row_lo + 31) / 32 * nseg;
-        const bool force = knob(KN_FORCE_TMA) != nullptr;
-        if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
+        // (no minimum work, unlike aligned rows: at 4096 x 4100 the ring is 4.74 us
+        // against K2 UNAL's 6.46 us)
+        if ((nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) && !knob(KN_TMA2_RSL32);
             const bool multi = o_packed != nullptr;
             return short_strips ? launch_tma2<8, true>(rp, multi, false, nseg, st)
@@ -251,7 +259,12 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
         rp.v8 = (a % 8 == 0 && !knob(KN_UNAL_BYTES)) ? 8
               : (a % 4 == 0 && !knob(KN_UNAL_BYTES)) ? 4 : 1;
     }
-    constexpr int rs = 4;
+    // 4-row strips; 2-row strips when that leaves fewer than 2 CTAs per SM
+    // (64 x 256 x 250: 128 CTAs of 4-row strips on 148 SMs)
+    int rs = 4;
+    if (((row_hi - row_lo + 3) / 4) * rp.items < (int64_t)sm_count() * 2 * kThreads &&
+        !knob(KN_UNAL_RS4))
+        rs = 2;
     rp.nstrips = (row_hi - row_lo + rs - 1) / rs;
     const int64_t grid = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
     if (grid > 0x7FFFFFFFLL) return kNoKernel;
