@@ -82,24 +82,16 @@ __device__ __forceinline__ uint32_t p4_get4(const uint8_t *in, int64_t off, int6
 
 // Thread = one 32-pixel word column of a strip of R rows (rows walked with the
 // up / centre / down words rolling in registers: one new row of 4 bytes per
-// output row), so the per-thread setup is paid once per R words.  The
-// horizontal neighbour pixels come from the neighbouring lanes' centre words
-// (a byte load only at warp edges), and the output -- rows start at any byte --
-// is realigned across lanes: with the row misaligned by m bytes, lane L stores
-// the aligned word holding lane L-1's last m bytes and its own first 4-m as
-// ONE 32-bit store; bytes no such store covers (row ends, warp edges) are
-// stored singly.  All lanes stay in the loop (shuffles), inactive ones store
-// nothing.
+// output row, plus the byte either side of the centre word for the horizontal
+// neighbours), so the per-thread setup is paid once per R words.
 template <int R>
 __global__ void __launch_bounds__(256)
 p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, WordGeom g,
                       int64_t rb, uint32_t nstrips, FastDiv dv_wp, FastDiv dv_h) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;    // < 2^32 (host check)
-    const int lane = threadIdx.x & 31;
-    const uint32_t strip_raw = fdiv(t, dv_wp);
-    const bool live = strip_raw < nstrips;
-    const uint32_t strip = live ? strip_raw : nstrips - 1;       // dead lanes mirror a valid strip
-    const int pw = (int)(t - strip_raw * (uint32_t)g.wp);
+    const uint32_t strip = fdiv(t, dv_wp);
+    if (strip >= nstrips) return;
+    const int pw = (int)(t - strip * (uint32_t)g.wp);
     const int64_t nbytes = g.nrows * rb;
     const uint32_t fw = g.fillword;
     const bool al = ((uintptr_t)in & 3) == 0;
@@ -109,9 +101,6 @@ p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
     // they are padding positions, forced below
     const uint32_t keep = nb == 4 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (8 * nb));
     const bool tail = pw == g.pl, has_r = b0 + 4 < rb;
-    // the previous / next lane holds the previous / next word of the same row
-    const bool prev_in = lane > 0 && pw > 0;
-    const bool next_in = lane < 31 && has_r;
     const uint32_t r0 = strip * R;                               // < 2^32 (host check)
     uint32_t y = r0 - fdiv(r0, dv_h) * (uint32_t)g.h;
     int64_t off = (int64_t)r0 * rb + b0;
@@ -123,16 +112,13 @@ p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
     uint32_t c = word(off);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-        const bool row_ok = live && r0 + i < g.nrows;
+        if (r0 + i >= g.nrows) break;
         const bool last = y == (uint32_t)g.h - 1;
         const uint32_t nx = r0 + i + 1 < g.nrows ? word(off + rb) : fw;
         const uint32_t d = last ? fw : nx;
-        // bit 0: pixel 32*pw - 1 (lane-1's bit 0); bit 31: pixel 32*pw + 32 (lane+1's bit 31)
-        const uint32_t cl = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-        const uint32_t cr = __shfl_down_sync(0xFFFFFFFFu, c, 1);
-        uint32_t lw = fw, rw = fw;
-        if (pw > 0) lw = prev_in ? cl : ~p4_ld8(in + off - 1);
-        if (has_r) rw = next_in ? cr : ~(p4_ld8(in + off + 4) << 24);
+        // its bit 0: pixel 32*pw - 1 (last bit of the byte before); bit 31: pixel 32*pw + 32
+        const uint32_t lw = pw > 0 ? ~p4_ld8(in + off - 1) : fw;
+        const uint32_t rw = has_r ? ~(p4_ld8(in + off + 4) << 24) : fw;
         const uint32_t ln = __funnelshift_r(c, lw, 1);
         uint32_t rn = __funnelshift_l(rw, c, 1);
         uint32_t f = 0u;
@@ -141,37 +127,13 @@ p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
             f = g.padmask;
         }
         const uint32_t e = ~(c | ~(ln | rn | up | d) | f);   // P4: 1 = black edge pixel
-        // ---- store: this row starts m bytes past a 4-byte boundary
-        const int m = (int)(((uintptr_t)out + (uintptr_t)(off - b0)) & 3);
-        const uint32_t ep = __shfl_up_sync(0xFFFFFFFFu, e, 1);
-        // lane L writes the aligned word [lane L-1's last m bytes | own first 4-m]
-        const bool whole = m != 0 && prev_in && nb >= 4 - m && row_ok;
-        const bool next_whole = __shfl_down_sync(0xFFFFFFFFu, whole ? 1 : 0, 1) != 0 && next_in;
         uint8_t *o = out + off;
-        if (row_ok) {
-            if (m == 0) {
-                if (nb == 4) {
-                    *reinterpret_cast<uint32_t *>(o) = __byte_perm(e, 0, 0x0123);   // P4 byte order
-                } else {
+        if (nb == 4 && ((uintptr_t)o & 3) == 0) {
+            *reinterpret_cast<uint32_t *>(o) = __byte_perm(e, 0, 0x0123);   // bytes in P4 order
+        } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (k < nb) o[k] = (uint8_t)(e >> (24 - 8 * k));
-                }
-            } else {
-                if (whole) {
-                    *reinterpret_cast<uint32_t *>(o - m) =
-                        __byte_perm(__funnelshift_r(e, ep, 8 * m), 0, 0x0123);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (k < nb && k < 4 - m) o[k] = (uint8_t)(e >> (24 - 8 * k));
-                }
-                if (!next_whole) {                // own last m bytes: no next-lane store covers them
-#pragma unroll
-                    for (int k = 1; k < 4; ++k)
-                        if (k >= 4 - m && k < nb) o[k] = (uint8_t)(e >> (24 - 8 * k));
-                }
-            }
+            for (int k = 0; k < 4; ++k)
+                if (k < nb) o[k] = (uint8_t)(e >> (24 - 8 * k));
         }
         up = last ? fw : c;                       // the next row starts a new image after `last`
         c = nx;
