@@ -40,7 +40,9 @@ HOT = [  # (label, substring of the demangled name)
     ("K1 H16 (16-byte rows, 8-word items)", "edge_reg_packed_kernel<0, 2, 8, 0, false, false, false, false, true>"),
     ("K1f flat (ragged packed rows)", "edge_flat_kernel<8, 0, 6, 0>"),
     ("K2w warp-per-image (C2 glyphs)", "edge_warp_img_kernel<1, 0, 8>"),
-    ("K2t2 TMA ring (C5 pages)", "edge_tma2_u8_kernel<8, 4, 0, false>"),
+    ("K2t2 TMA ring (C5 pages)", "edge_tma2_u8_kernel<8, 4, 0, false, false>"),
+    ("K2t2 UNAL (uint8 rows at byte offsets)", "edge_tma2_u8_kernel<8, 4, 0, false, true>"),
+    ("K1s flat ring (opt-in)", "edge_flat_ring_kernel<0, 0, 11>"),
     ("K2 (uint8 -> u64 drop-in, small images)", "edge_reg_u8_kernel<4, 0, false, true, 0>"),
 ]
 
