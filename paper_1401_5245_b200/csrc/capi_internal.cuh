@@ -55,6 +55,7 @@ enum Knob : int {
     KN_NO_H16,
     KN_RING,
     KN_NO_TMA_UNAL,
+    KN_P4_NO_FLAT,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

@@ -142,6 +142,162 @@ p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
     }
 }
 
+// K1p: P4 payloads whose rows are not whole 4-byte words, viewed -- like K1f --
+// as ONE flat byte array (rows of rb bytes back to back): thread = one aligned
+// 16-byte chunk; the rows above / below are the bytes rb before / after, at a
+// fixed byte phase from the chunk grid (RDW words + s bytes: RDW a template
+// constant, s uniform), taken from the lane's own aligned chunk and the next
+// lane's by funnel shifts; the neighbour pixels from the neighbouring lanes
+// (a byte load at warp edges).  Row boundaries fall inside words at byte
+// granularity, so each word gets its row structure as bit masks (first pixel
+// of a row: left fill; pixel w-1: right fill; padding bits; top / bottom row
+// of an image: vertical fill).  The output has the input's flat layout, so
+// every store is one aligned 16-byte store -- no row is ever written by two
+// threads.  Chunks within two rows of the buffer ends load byte by byte.
+struct P4FlatParams {
+    const uint8_t *in;       // 16-byte aligned
+    uint8_t *out;            // 16-byte aligned
+    uint32_t nbytes;         // nrows * rb < 2^31
+    uint32_t rb, h, nchunks;
+    uint32_t wlast;          // (w - 1) % 8: bit of pixel w-1 in its byte (MSB = 0)
+    uint32_t fw;
+    int s;                   // rb % 4 (byte part of the down phase)
+    FastDiv div_rb, div_h;
+};
+
+__device__ __forceinline__ uint32_t p4w(uint32_t mem) {            // P4 LE word -> white, pixel order
+    return ~__byte_perm(mem, 0, 0x0123);
+}
+
+template <int RDW>
+__global__ void __launch_bounds__(256)
+p4_flat_kernel(const P4FlatParams p) {
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool live = t < p.nchunks;
+    const uint32_t q = live ? t : p.nchunks - 1;
+    const int64_t base = (int64_t)q * 16;
+    const int64_t rb = p.rb, nb = p.nbytes;
+    const int64_t full = nb / 16;
+    auto chunk = [&](int64_t b0, uint32_t (&v)[4]) {   // clamped aligned 16-byte chunk
+        int64_t c = b0 >= 0 ? b0 / 16 : 0;
+        c = c >= full ? full - 1 : c;
+        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p.in + c * 16));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    };
+    // down phase RD = rb % 16 = 4 * RDW + s; up phase RU = (16 - RD) % 16
+    const int s = p.s;
+    const int RD = 4 * RDW + s;
+    const int RU = (16 - RD) & 15;
+    uint32_t u0[4], cm[4], d0[4];
+    chunk(base - rb - RU, u0);
+    chunk(base, cm);
+    chunk(base + rb - RD, d0);
+    // (u0 ++ next lane's u0) from byte RU; (d0 ++ next lane's d0) from byte RD
+    uint32_t un[4], dn[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        un[j] = __shfl_down_sync(0xFFFFFFFFu, u0[j], 1);
+        dn[j] = __shfl_down_sync(0xFFFFFFFFu, d0[j], 1);
+    }
+    if (lane == 31) {               // the next warp's lane 0 chunks
+        chunk(base - rb - RU + 16, un);
+        chunk(base + rb - RD + 16, dn);
+    }
+    uint32_t up[4], dw[4];
+    {
+        const uint32_t U[8] = {u0[0], u0[1], u0[2], u0[3], un[0], un[1], un[2], un[3]};
+        const uint32_t D[8] = {d0[0], d0[1], d0[2], d0[3], dn[0], dn[1], dn[2], dn[3]};
+        // up: word offset RU / 4 (RU = 16 - RD: 4 - RDW words if s == 0, else 3 - RDW)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            dw[j] = __funnelshift_r(D[j + RDW], D[j + RDW + 1 < 8 ? j + RDW + 1 : 7], 8 * s);
+            const uint32_t a0 = s == 0 ? U[(j + 4 - RDW) & 7] : U[j + 3 - RDW];
+            const uint32_t a1 = s == 0 ? a0 : U[j + 4 - RDW < 8 ? j + 4 - RDW : 7];
+            up[j] = s == 0 ? a0 : __funnelshift_r(a0, a1, 8 * ((4 - s) & 3));
+        }
+    }
+    // chunks near the buffer ends (clamped vector loads) and the ragged tail: bytes
+    const bool edge_zone = base < rb + 32 || base + rb + 32 > nb || base + 16 > nb;
+    if (edge_zone) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t c = 0u, uu = 0u, dd = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t b = base + 4 * j + k;
+                if (b < nb) c |= (uint32_t)p.in[b] << (8 * k);
+                if (b - rb >= 0 && b - rb < nb) uu |= (uint32_t)p.in[b - rb] << (8 * k);
+                if (b + rb < nb) dd |= (uint32_t)p.in[b + rb] << (8 * k);
+            }
+            cm[j] = c; up[j] = uu; dw[j] = dd;
+        }
+    }
+    // white-domain pixel-order words; neighbours across lanes
+    uint32_t c[4], cu[4], cd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        c[j] = p4w(cm[j]);
+        cu[j] = p4w(up[j]);
+        cd[j] = p4w(dw[j]);
+    }
+    uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, c[3], 1);    // bit 0: the pixel before the chunk
+    uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, c[0], 1);  // bit 31: the pixel after
+    if (lane == 0) lw = base > 0 ? ~(uint32_t)p.in[base - 1] : 0u;
+    if (lane == 31) rw = base + 16 < nb ? ~((uint32_t)p.in[base + 16] << 24) : 0u;
+    if (!live) return;
+
+    // row structure: byte jb of row r starts the chunk; words advance 4 bytes
+    uint32_t r = fdiv((uint32_t)base, p.div_rb);
+    uint32_t jb = (uint32_t)base - r * p.rb;
+    uint32_t y = r - fdiv(r, p.div_h) * p.h;
+    const uint32_t fw = p.fw;
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (j > 0) {
+            jb += 4;
+            if (jb >= p.rb) {                 // rb >= 4: at most one row start per word
+                jb -= p.rb;
+                y = y + 1 == p.h ? 0u : y + 1;
+            }
+        }
+        const uint32_t eb = p.rb - jb;        // bytes left in row r from this word's byte 0
+        const uint32_t y1 = y + 1 == p.h ? 0u : y + 1;
+        // bits of the bytes that belong to row r + 1 (eb < 4)
+        const uint32_t nxt = eb < 4 ? (0xFFFFFFFFu >> (8 * eb)) : 0u;
+        uint32_t lfix = jb == 0 ? 0x80000000u : 0u;            // first pixel of a row
+        if (eb < 4) lfix |= 0x80000000u >> (8 * eb);
+        uint32_t rfix = 0u, pad = 0u;                          // pixel w-1 / padding of row r
+        if (eb <= 4) {
+            const uint32_t bit = 31 - 8 * (eb - 1) - p.wlast;  // pixel w-1
+            rfix = 1u << bit;
+            pad = (rfix - 1u) & (0xFFFFFFFFu >> (8 * (eb - 1))) & ~nxt;
+        }
+        const uint32_t umask = (y == 0 ? ~nxt : 0u) | (y1 == 0 ? nxt : 0u);
+        const uint32_t dmask = (y == p.h - 1 ? ~nxt : 0u) | (y1 == p.h - 1 ? nxt : 0u);
+        const uint32_t left = j == 0 ? lw : c[j - 1];
+        const uint32_t right = j == 3 ? rw : c[j + 1];
+        const uint32_t ln = (__funnelshift_r(c[j], left, 1) & ~lfix) | (fw & lfix);
+        const uint32_t rn = (__funnelshift_l(right, c[j], 1) & ~rfix) | (fw & rfix);
+        const uint32_t u = (cu[j] & ~umask) | (fw & umask);
+        const uint32_t d = (cd[j] & ~dmask) | (fw & dmask);
+        const uint32_t e = c[j] | ~(ln | rn | u | d) | pad;    // white domain, padding 1
+        o[j] = __byte_perm(~e, 0, 0x0123);                      // P4: 1 = black, padding 0
+    }
+    if (base + 16 <= nb) {
+        *reinterpret_cast<uint4 *>(p.out + base) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (base + 4 * j + k < nb) p.out[base + 4 * j + k] = (uint8_t)(o[j] >> (8 * k));
+    }
+}
+
 }  // namespace capi
 }  // namespace bitedge
 
@@ -234,6 +390,30 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
                          st, rp, dv);
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
+    }
+    // any other row length >= 4 bytes, 16-byte aligned buffers: K1p (the payload
+    // as one flat byte array, aligned 16-byte loads and stores)
+    if (rb >= 4 && al(p4_in, 16) && al(p4_out, 16) && n * h * rb < ((int64_t)1 << 31) - 64 &&
+        !knob(KN_P4_UNFUSED) && !knob(KN_P4_BYTES) && !knob(KN_P4_NO_FLAT)) {
+        P4FlatParams fp;
+        memset(&fp, 0, sizeof(fp));
+        fp.in = p4_in; fp.out = p4_out;
+        fp.nbytes = (uint32_t)(n * h * rb);
+        fp.rb = (uint32_t)rb; fp.h = (uint32_t)h;
+        fp.nchunks = (fp.nbytes + 15) / 16;
+        fp.wlast = (uint32_t)((w - 1) % 8);
+        fp.fw = G.fillword;
+        fp.s = (int)(rb % 4);
+        fp.div_rb = make_fastdiv((uint32_t)rb);
+        fp.div_h = make_fastdiv((uint32_t)h);
+        const unsigned grid = (fp.nchunks + 255) / 256;
+        switch ((int)((rb % 16) / 4)) {
+            case 0: launch_kb(p4_flat_kernel<0>, grid, 256u, 0, st, fp); break;
+            case 1: launch_kb(p4_flat_kernel<1>, grid, 256u, 0, st, fp); break;
+            case 2: launch_kb(p4_flat_kernel<2>, grid, 256u, 0, st, fp); break;
+            default: launch_kb(p4_flat_kernel<3>, grid, 256u, 0, st, fp); break;
+        }
+        return cuda_check("p4_flat_kernel");
     }
     // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items cut
     // out of aligned 16-byte chunks (UNAL)

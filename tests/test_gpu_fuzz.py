@@ -73,7 +73,8 @@ def test_fuzz(seed, cuda_dev, monkeypatch):
             monkeypatch.delenv(k, raising=False)
 
 
-@pytest.mark.parametrize("knob", [None, "BITEDGE_P4_BYTES", "BITEDGE_P4_UNFUSED"])
+@pytest.mark.parametrize("knob", [None, "BITEDGE_P4_BYTES", "BITEDGE_P4_UNFUSED",
+                                  "BITEDGE_P4_NO_FLAT"])
 @pytest.mark.parametrize("seed", range(4))
 def test_fuzz_p4(seed, knob, cuda_dev, monkeypatch):
     import torch
@@ -146,3 +147,33 @@ def test_fuzz_halo_slabs_all_inputs(knob, cuda_dev, monkeypatch):
                 else:
                     got = got.view(np.uint32)
                 assert (got == ex).all(), (knob, name, k, H, W, cuts)
+
+
+@pytest.mark.parametrize("w", [25, 31, 33, 57, 100, 127, 129, 250, 255, 257, 1000, 1001, 2047,
+                               4100, 8001, 32002])
+def test_p4_flat_widths(w, cuda_dev, monkeypatch):
+    """K1p (P4 payloads viewed as one flat byte array) for every row-length
+    phase mod 16 bytes, batches whose images start mid-word, h = 1 / 2 / many,
+    both borders -- against the oracle and against the byte kernel."""
+    import torch
+
+    from paper_1401_5245_b200 import pbm
+
+    rng = np.random.default_rng(w)
+    rb = (w + 7) // 8
+    for n, h in ((1, 1), (1, 2), (3, 7), (2, 40)) if w < 8000 else ((1, 3), (2, 9)):
+        a = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
+        bits = rng.integers(0, 2, (n, h, rb * 8)).astype(np.uint8)   # garbage padding bits
+        bits[..., :w] = a
+        payload = torch.from_numpy(np.packbits(1 - bits, axis=-1).reshape(-1).copy()).to(cuda_dev)
+        for fill in (1, 0):
+            out = pbm.detect_p4(payload, n, h, w, fill).cpu().numpy().reshape(n, h, rb)
+            got = 1 - np.unpackbits(out, axis=-1)[..., :w]
+            exp = P.unpack_u32(cscan.scan_u8(a, fill), w)
+            assert (got == exp).all(), (n, h, w, fill)
+            if w % 8:
+                assert not (out[..., -1] & ((1 << (8 - w % 8)) - 1)).any()
+            monkeypatch.setenv("BITEDGE_P4_BYTES", "1")
+            ref = pbm.detect_p4(payload, n, h, w, fill).cpu().numpy().reshape(n, h, rb)
+            monkeypatch.delenv("BITEDGE_P4_BYTES")
+            assert (ref == out).all(), (n, h, w, fill)
