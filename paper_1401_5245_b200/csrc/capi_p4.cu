@@ -391,9 +391,17 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }
-    // any other row length >= 4 bytes, 16-byte aligned buffers: K1p (the payload
-    // as one flat byte array, aligned 16-byte loads and stores)
-    if (rb >= 4 && al(p4_in, 16) && al(p4_out, 16) && n * h * rb < ((int64_t)1 << 31) - 64 &&
+    // byte-granular rows (rb % 4 != 0) >= 4 bytes, 16-byte aligned buffers up to
+    // kP4FlatMax bytes: K1p (the payload as one flat byte array, aligned 16-byte
+    // loads and stores).  Measured: 2000x2000 (250-byte rows) 4.49 -> 2.65 us
+    // against the byte kernel, 8000x8001 10.8 -> 10.2 us, 12000x12002 even; from
+    // 16000x16002 (32 MB) up the byte kernel is faster (32.0 vs 33.3 us; 32000x32002
+    // 113 vs 126 us), and rows of whole 4-byte words run K1 UNAL below (8000x8000:
+    // 7.0 us vs K1p 10.2 us).
+    constexpr int64_t kP4FlatMax = (int64_t)24 << 20;
+    const int64_t p4_bytes = n * h * rb;
+    if (rb >= 4 && rb % 4 != 0 && p4_bytes >= 16 && p4_bytes <= kP4FlatMax &&
+        al(p4_in, 16) && al(p4_out, 16) &&
         !knob(KN_P4_UNFUSED) && !knob(KN_P4_BYTES) && !knob(KN_P4_NO_FLAT)) {
         P4FlatParams fp;
         memset(&fp, 0, sizeof(fp));

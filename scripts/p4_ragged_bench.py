@@ -12,7 +12,7 @@ from paper_1401_5245_b200 import _capi  # noqa: E402
 from paper_1401_5245_b200 import pbm  # noqa: E402
 
 dev = torch.device("cuda:0")
-for (h, w) in ((32000, 32000), (32000, 31993), (32000, 32002), (8000, 8000), (8000, 7993), (2000, 2000), (256, 250)):
+for (h, w) in ((32000, 32000), (32000, 31993), (32000, 32002), (16000, 16002), (12000, 12002), (8000, 8001), (8000, 8000), (8000, 7993), (2000, 2000), (256, 250)):
     rb = (w + 7) // 8
     nbytes = h * rb
     pool = max(2, min(32, (3 * 126 << 20) // (2 * nbytes) + 1))
