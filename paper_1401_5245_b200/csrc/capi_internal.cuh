@@ -56,6 +56,9 @@ enum Knob : int {
     KN_RING,
     KN_NO_TMA_UNAL,
     KN_P4_NO_FLAT,
+    KN_P4_FLAT16,
+    KN_P4_FLAT_MAX,
+    KN_P4_FLAT32,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

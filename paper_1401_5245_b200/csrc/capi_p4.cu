@@ -2,6 +2,7 @@
 // decode / encode kernels and the fused P4 -> edges -> P4 path through K1.
 #include "capi_internal.cuh"
 #include "edge_reg.cuh"
+#include "edge_flat.cuh"
 
 using namespace bitedge;
 using namespace bitedge::capi;
@@ -144,19 +145,28 @@ p4_edges_bytes_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
 
 // K1p: P4 payloads whose rows are not whole 4-byte words, viewed -- like K1f --
 // as ONE flat byte array (rows of rb bytes back to back): thread = one aligned
-// 16-byte chunk; the rows above / below are the bytes rb before / after, at a
-// fixed byte phase from the chunk grid (RDW words + s bytes: RDW a template
-// constant, s uniform), taken from the lane's own aligned chunk and the next
-// lane's by funnel shifts; the neighbour pixels from the neighbouring lanes
-// (a byte load at warp edges).  Row boundaries fall inside words at byte
-// granularity, so each word gets its row structure as bit masks (first pixel
-// of a row: left fill; pixel w-1: right fill; padding bits; top / bottom row
-// of an image: vertical fill).  The output has the input's flat layout, so
-// every store is one aligned 16-byte store -- no row is ever written by two
-// threads.  Chunks within two rows of the buffer ends load byte by byte.
+// chunk of CW words (32 bytes when the buffers are 32-byte aligned, else 16);
+// the rows above / below are the bytes rb before / after, at a fixed byte phase
+// from the chunk grid (RDW words + s bytes: RDW a template constant, s
+// uniform), taken from the lane's own aligned chunk and the next lane's by
+// funnel shifts; the neighbour pixels from the neighbouring lanes (a byte load
+// at warp edges).  The output has the input's flat layout, so every store is
+// one aligned vector store -- no row is ever written by two threads.
+//
+// Row boundaries fall inside words at byte granularity, but only in the one or
+// two chunks per row that hold a row's first or last byte.  Every other chunk
+// ("plain") is evaluated in the P4 domain as loaded (1 = black; AND / OR / NOT
+// commute with the byte reversal, so only the two horizontal shifts run in
+// pixel order): out = c & ~(pi(L & R) & u & d), ~10 instructions per word.  A
+// chunk with a row boundary tests each of its words; the word holding a row's
+// first / last byte gets its row structure as bit masks (first pixel of a row:
+// left fill; pixel w-1: right fill; padding bits; top / bottom row of an image:
+// vertical fill).  Before the split every word paid for the masks (~55
+// instructions: issue-bound, 2.0 TB/s at 32000x32002).  Chunks within two rows
+// of the buffer ends load byte by byte.
 struct P4FlatParams {
-    const uint8_t *in;       // 16-byte aligned
-    uint8_t *out;            // 16-byte aligned
+    const uint8_t *in;       // 4*CW-byte aligned
+    uint8_t *out;            // 4*CW-byte aligned
     uint32_t nbytes;         // nrows * rb < 2^31
     uint32_t rb, h, nchunks;
     uint32_t wlast;          // (w - 1) % 8: bit of pixel w-1 in its byte (MSB = 0)
@@ -169,65 +179,144 @@ __device__ __forceinline__ uint32_t p4w(uint32_t mem) {            // P4 LE word
     return ~__byte_perm(mem, 0, 0x0123);
 }
 
-template <int RDW>
-__global__ void __launch_bounds__(256)
-p4_flat_kernel(const P4FlatParams p) {
+// One word that holds a row's first and / or last byte, or lies in an image's top /
+// bottom row: its row structure as bit masks, white domain.  cbj / left / right:
+// black-domain pixel-order words (left: bit 0 = the pixel before, right: bit 31 = the
+// pixel after); upm / dwm: the words rb bytes before / after, as loaded; jb: the byte
+// of its row the word starts at; y: that row's index in its image.
+__device__ __forceinline__ uint32_t p4_row_word(const P4FlatParams &p, uint32_t cbj, uint32_t left,
+                                                uint32_t right, uint32_t upm, uint32_t dwm,
+                                                uint32_t jb, uint32_t y) {
+    const uint32_t fw = p.fw, hm1 = p.h - 1;
+    const uint32_t eb = p.rb - jb;            // bytes left in the row from this word's byte 0
+    const uint32_t y1 = y == hm1 ? 0u : y + 1;
+    // bits of the bytes that belong to the next row (eb < 4)
+    const uint32_t nxt = eb < 4 ? (0xFFFFFFFFu >> (8 * eb)) : 0u;
+    uint32_t lfix = jb == 0 ? 0x80000000u : 0u;            // first pixel of a row
+    if (eb < 4) lfix |= 0x80000000u >> (8 * eb);
+    uint32_t rfix = 0u, pad = 0u;                          // pixel w-1 / padding of the row
+    if (eb <= 4) {
+        const uint32_t bit = 31 - 8 * (eb - 1) - p.wlast;  // pixel w-1
+        rfix = 1u << bit;
+        pad = (rfix - 1u) & (0xFFFFFFFFu >> (8 * (eb - 1))) & ~nxt;
+    }
+    const uint32_t umask = (y == 0 ? ~nxt : 0u) | (y1 == 0 ? nxt : 0u);
+    const uint32_t dmask = (y == hm1 ? ~nxt : 0u) | (y1 == hm1 ? nxt : 0u);
+    const uint32_t c = ~cbj;
+    const uint32_t ln = (__funnelshift_r(c, ~left, 1) & ~lfix) | (fw & lfix);
+    const uint32_t rn = (__funnelshift_l(~right, c, 1) & ~rfix) | (fw & rfix);
+    const uint32_t u = (p4w(upm) & ~umask) | (fw & umask);
+    const uint32_t d = (p4w(dwm) & ~dmask) | (fw & dmask);
+    const uint32_t e = c | ~(ln | rn | u | d) | pad;      // white domain, padding 1
+    return __byte_perm(~e, 0, 0x0123);                    // P4: 1 = black, padding 0
+}
+
+// A chunk near the buffer ends (where the clamped vector loads do not cover what it
+// needs) or the ragged last chunk, word by word from byte loads; out of line.
+__device__ __noinline__ void p4_flat_edge_chunk(const P4FlatParams &p, int base, int cw,
+                                                uint32_t jb, uint32_t y) {
+    const int rb = (int)p.rb, nb = (int)p.nbytes;
+#pragma unroll 1
+    for (int j = 0; j < cw; ++j) {
+        const int b0 = base + 4 * j;
+        if (b0 >= nb) break;
+        if (j > 0) {
+            jb += 4;
+            while (jb >= p.rb) {
+                jb -= p.rb;
+                y = y == p.h - 1 ? 0u : y + 1;
+            }
+        }
+        uint32_t c = 0u, uu = 0u, dd = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int b = b0 + k;
+            if (b < nb) c |= (uint32_t)p.in[b] << (8 * k);
+            if (b - rb >= 0 && b - rb < nb) uu |= (uint32_t)p.in[b - rb] << (8 * k);
+            if (b + rb < nb) dd |= (uint32_t)p.in[b + rb] << (8 * k);
+        }
+        const uint32_t left = b0 > 0 ? (uint32_t)p.in[b0 - 1] : 0u;
+        const uint32_t right = b0 + 4 < nb ? (uint32_t)p.in[b0 + 4] << 24 : 0u;
+        const uint32_t o = p4_row_word(p, __byte_perm(c, 0, 0x0123), left, right, uu, dd, jb, y);
+        if (b0 + 4 <= nb) {
+            *reinterpret_cast<uint32_t *>(p.out + b0) = o;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (b0 + k < nb) p.out[b0 + k] = (uint8_t)(o >> (8 * k));
+        }
+    }
+}
+
+template <int CW, int RDW, bool EDGE_INLINE>
+__global__ void __launch_bounds__(256, CW == 8 ? 5 : 0)
+p4_flat_kernel(const __grid_constant__ P4FlatParams p) {
+    constexpr int CB = 4 * CW;
+    constexpr int LCB = CW == 8 ? 5 : 4;
     pdl_wait();
     pdl_trigger();
-    const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+    // a warp owns 31 consecutive chunks; lane 31 only loads and shuffles the chunk after
+    // them (the next warp's first), so no lane reloads a neighbour's chunks
     const int lane = threadIdx.x & 31;
-    const bool live = t < p.nchunks;
-    const uint32_t q = live ? t : p.nchunks - 1;
-    const int64_t base = (int64_t)q * 16;
-    const int64_t rb = p.rb, nb = p.nbytes;
-    const int64_t full = nb / 16;
-    auto chunk = [&](int64_t b0, uint32_t (&v)[4]) {   // clamped aligned 16-byte chunk
-        int64_t c = b0 >= 0 ? b0 / 16 : 0;
-        c = c >= full ? full - 1 : c;
-        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p.in + c * 16));
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    const uint32_t t = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 31 + lane;
+    const bool live = lane < 31 && t < p.nchunks;
+    const uint32_t q = t < p.nchunks ? t : p.nchunks - 1;
+    const int base = (int)(q * CB);                     // nbytes <= 2^30: 32-bit byte offsets
+    const int rb = (int)p.rb, nb = (int)p.nbytes;
+    const int full = nb >> LCB;
+    auto chunk = [&](int b0, uint32_t (&v)[CW]) {       // clamped aligned chunk
+        const int c = min(max(b0 >> LCB, 0), full - 1);
+        flat_load<CW>(reinterpret_cast<const uint32_t *>(p.in + (size_t)c * CB), v);
     };
-    // down phase RD = rb % 16 = 4 * RDW + s; up phase RU = (16 - RD) % 16
+    // down phase RD = rb % CB = 4 * RDW + s (s = rb % 4 in 1..3); up phase RU = CB - RD
     const int s = p.s;
     const int RD = 4 * RDW + s;
-    const int RU = (16 - RD) & 15;
-    uint32_t u0[4], cm[4], d0[4];
+    const int RU = CB - RD;
+    uint32_t u0[CW], cm[CW], d0[CW];
     chunk(base - rb - RU, u0);
     chunk(base, cm);
     chunk(base + rb - RD, d0);
-    // (u0 ++ next lane's u0) from byte RU; (d0 ++ next lane's d0) from byte RD
-    uint32_t un[4], dn[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        un[j] = __shfl_down_sync(0xFFFFFFFFu, u0[j], 1);
-        dn[j] = __shfl_down_sync(0xFFFFFFFFu, d0[j], 1);
-    }
-    if (lane == 31) {               // the next warp's lane 0 chunks
-        chunk(base - rb - RU + 16, un);
-        chunk(base + rb - RD + 16, dn);
-    }
-    uint32_t up[4], dw[4];
+    uint32_t lwb = 0u;                                  // the byte before the warp's chunks
+    if (lane == 0 && base > 0) lwb = p4_ld8(p.in + base - 1);
+    // (u0 ++ next lane's u0) from byte RU = 4 * (CW - 1 - RDW) + (4 - s); (d0 ++ next
+    // lane's d0) from byte RD: one funnel shift per word
+    uint32_t up[CW], dw[CW];
     {
-        const uint32_t U[8] = {u0[0], u0[1], u0[2], u0[3], un[0], un[1], un[2], un[3]};
-        const uint32_t D[8] = {d0[0], d0[1], d0[2], d0[3], dn[0], dn[1], dn[2], dn[3]};
-        // up: word offset RU / 4 (RU = 16 - RD: 4 - RDW words if s == 0, else 3 - RDW)
+        uint32_t U[2 * CW];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            dw[j] = __funnelshift_r(D[j + RDW], D[j + RDW + 1 < 8 ? j + RDW + 1 : 7], 8 * s);
-            const uint32_t a0 = s == 0 ? U[(j + 4 - RDW) & 7] : U[j + 3 - RDW];
-            const uint32_t a1 = s == 0 ? a0 : U[j + 4 - RDW < 8 ? j + 4 - RDW : 7];
-            up[j] = s == 0 ? a0 : __funnelshift_r(a0, a1, 8 * ((4 - s) & 3));
+        for (int j = 0; j < CW; ++j) {
+            U[j] = u0[j];
+            U[CW + j] = __shfl_down_sync(0xFFFFFFFFu, u0[j], 1);
         }
-    }
-    // chunks near the buffer ends (clamped vector loads) and the ragged tail: bytes
-    const bool edge_zone = base < rb + 32 || base + rb + 32 > nb || base + 16 > nb;
-    if (edge_zone) {
+        const uint32_t su = 32 - 8 * s;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CW; ++j)
+            up[j] = __funnelshift_r(U[j + CW - 1 - RDW], U[j + CW - RDW], su);
+    }
+    {
+        uint32_t D[2 * CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            D[j] = d0[j];
+            D[CW + j] = __shfl_down_sync(0xFFFFFFFFu, d0[j], 1);
+        }
+        const uint32_t sd = 8 * s;
+#pragma unroll
+        for (int j = 0; j < CW; ++j)
+            dw[j] = __funnelshift_r(D[j + RDW], D[j + RDW + 1], sd);
+    }
+    // chunks within two rows of the buffer ends (clamped vector loads) and the ragged
+    // tail.  EDGE_INLINE (small payloads, where the slowest warp is the kernel time):
+    // reload their words from bytes here, all loads in flight at once; otherwise they are
+    // redone out of line below, keeping this code out of the large rasters' main path
+    const bool edge_zone = base < rb + 2 * CB || base + rb + 2 * CB > nb || base + CB > nb;
+    if (EDGE_INLINE && edge_zone) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
             uint32_t c = 0u, uu = 0u, dd = 0u;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const int64_t b = base + 4 * j + k;
+                const int b = base + 4 * j + k;
                 if (b < nb) c |= (uint32_t)p.in[b] << (8 * k);
                 if (b - rb >= 0 && b - rb < nb) uu |= (uint32_t)p.in[b - rb] << (8 * k);
                 if (b + rb < nb) dd |= (uint32_t)p.in[b + rb] << (8 * k);
@@ -235,63 +324,56 @@ p4_flat_kernel(const P4FlatParams p) {
             cm[j] = c; up[j] = uu; dw[j] = dd;
         }
     }
-    // white-domain pixel-order words; neighbours across lanes
-    uint32_t c[4], cu[4], cd[4];
+    // black-domain pixel-order centre words; neighbours across lanes
+    uint32_t cb[CW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        c[j] = p4w(cm[j]);
-        cu[j] = p4w(up[j]);
-        cd[j] = p4w(dw[j]);
-    }
-    uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, c[3], 1);    // bit 0: the pixel before the chunk
-    uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, c[0], 1);  // bit 31: the pixel after
-    if (lane == 0) lw = base > 0 ? ~(uint32_t)p.in[base - 1] : 0u;
-    if (lane == 31) rw = base + 16 < nb ? ~((uint32_t)p.in[base + 16] << 24) : 0u;
+    for (int j = 0; j < CW; ++j) cb[j] = __byte_perm(cm[j], 0, 0x0123);
+    uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cb[CW - 1], 1);   // bit 0: the pixel before the chunk
+    const uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cb[0], 1);  // bit 31: the pixel after
+    if (lane == 0) lw = lwb;
     if (!live) return;
 
-    // row structure: byte jb of row r starts the chunk; words advance 4 bytes
-    uint32_t r = fdiv((uint32_t)base, p.div_rb);
+    // ---- every word as a word inside its row, inside its image (P4 domain)
+    uint32_t o[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+        const uint32_t left = j == 0 ? lw : cb[j - 1];
+        const uint32_t right = j == CW - 1 ? rw : cb[j + 1];
+        const uint32_t lr = __funnelshift_r(cb[j], left, 1) & __funnelshift_l(right, cb[j], 1);
+        o[j] = cm[j] & ~(__byte_perm(lr, 0, 0x0123) & up[j] & dw[j]);
+    }
+    // ---- row structure: byte jb of row r starts the chunk
+    const uint32_t r = fdiv((uint32_t)base, p.div_rb);
     uint32_t jb = (uint32_t)base - r * p.rb;
     uint32_t y = r - fdiv(r, p.div_h) * p.h;
-    const uint32_t fw = p.fw;
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (j > 0) {
-            jb += 4;
-            if (jb >= p.rb) {                 // rb >= 4: at most one row start per word
-                jb -= p.rb;
-                y = y + 1 == p.h ? 0u : y + 1;
-            }
-        }
-        const uint32_t eb = p.rb - jb;        // bytes left in row r from this word's byte 0
-        const uint32_t y1 = y + 1 == p.h ? 0u : y + 1;
-        // bits of the bytes that belong to row r + 1 (eb < 4)
-        const uint32_t nxt = eb < 4 ? (0xFFFFFFFFu >> (8 * eb)) : 0u;
-        uint32_t lfix = jb == 0 ? 0x80000000u : 0u;            // first pixel of a row
-        if (eb < 4) lfix |= 0x80000000u >> (8 * eb);
-        uint32_t rfix = 0u, pad = 0u;                          // pixel w-1 / padding of row r
-        if (eb <= 4) {
-            const uint32_t bit = 31 - 8 * (eb - 1) - p.wlast;  // pixel w-1
-            rfix = 1u << bit;
-            pad = (rfix - 1u) & (0xFFFFFFFFu >> (8 * (eb - 1))) & ~nxt;
-        }
-        const uint32_t umask = (y == 0 ? ~nxt : 0u) | (y1 == 0 ? nxt : 0u);
-        const uint32_t dmask = (y == p.h - 1 ? ~nxt : 0u) | (y1 == p.h - 1 ? nxt : 0u);
-        const uint32_t left = j == 0 ? lw : c[j - 1];
-        const uint32_t right = j == 3 ? rw : c[j + 1];
-        const uint32_t ln = (__funnelshift_r(c[j], left, 1) & ~lfix) | (fw & lfix);
-        const uint32_t rn = (__funnelshift_l(right, c[j], 1) & ~rfix) | (fw & rfix);
-        const uint32_t u = (cu[j] & ~umask) | (fw & umask);
-        const uint32_t d = (cd[j] & ~dmask) | (fw & dmask);
-        const uint32_t e = c[j] | ~(ln | rn | u | d) | pad;    // white domain, padding 1
-        o[j] = __byte_perm(~e, 0, 0x0123);                      // P4: 1 = black, padding 0
+    const uint32_t hm1 = p.h - 1;
+    // out-of-line edge chunks (their loads and shuffles above served the neighbours)
+    if (!EDGE_INLINE && edge_zone) {
+        p4_flat_edge_chunk(p, base, CW, jb, y);
+        return;
     }
-    if (base + 16 <= nb) {
-        *reinterpret_cast<uint4 *>(p.out + base) = make_uint4(o[0], o[1], o[2], o[3]);
+    // chunks holding a row's first or last byte, or in an image's top / bottom row,
+    // redo the words concerned
+    if (jb == 0 || jb + CB >= p.rb || y == 0 || y == hm1) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            if (j > 0) {
+                jb += 4;
+                if (jb >= p.rb) {                 // rb >= 4: at most one row start per word
+                    jb -= p.rb;
+                    y = y == hm1 ? 0u : y + 1;
+                }
+            }
+            if (jb != 0 && p.rb - jb > 4 && y != 0 && y != hm1) continue;
+            o[j] = p4_row_word(p, cb[j], j == 0 ? lw : cb[j - 1], j == CW - 1 ? rw : cb[j + 1],
+                               up[j], dw[j], jb, y);
+        }
+    }
+    if (!EDGE_INLINE || base + CB <= nb) {
+        store_chunk<CW>(reinterpret_cast<uint32_t *>(p.out + base), o);
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < CW; ++j)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (base + 4 * j + k < nb) p.out[base + 4 * j + k] = (uint8_t)(o[j] >> (8 * k));
@@ -391,36 +473,48 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
             return cuda_check("edge_reg_packed_kernel<P4>");
         }
     }
-    // byte-granular rows (rb % 4 != 0) >= 4 bytes, 16-byte aligned buffers up to
-    // kP4FlatMax bytes: K1p (the payload as one flat byte array, aligned 16-byte
-    // loads and stores).  Measured: 2000x2000 (250-byte rows) 4.49 -> 2.65 us
-    // against the byte kernel, 8000x8001 10.8 -> 10.2 us, 12000x12002 even; from
-    // 16000x16002 (32 MB) up the byte kernel is faster (32.0 vs 33.3 us; 32000x32002
-    // 113 vs 126 us), and rows of whole 4-byte words run K1 UNAL below (8000x8000:
-    // 7.0 us vs K1p 10.2 us).
-    constexpr int64_t kP4FlatMax = (int64_t)24 << 20;
+    // byte-granular rows (rb % 4 != 0) >= 4 bytes in 16-byte aligned buffers: K1p (the
+    // payload as one flat byte array, aligned vector loads and stores; 32-byte
+    // chunks when both buffers allow, BITEDGE_P4_FLAT16 keeps 16-byte chunks;
+    // BITEDGE_P4_FLAT_MAX caps the payload size in bytes).  Rows of whole 4-byte
+    // words run K1 UNAL below (8000x8000: 7.0 us).
+    int64_t flat_max = (int64_t)1 << 30;                   // 32-bit byte offsets in the kernel
+    if (const char *v = knob(KN_P4_FLAT_MAX)) flat_max = atoll(v);
     const int64_t p4_bytes = n * h * rb;
-    if (rb >= 4 && rb % 4 != 0 && p4_bytes >= 16 && p4_bytes <= kP4FlatMax &&
+    if (rb >= 4 && rb % 4 != 0 && p4_bytes >= 32 && p4_bytes <= flat_max &&
         al(p4_in, 16) && al(p4_out, 16) &&
         !knob(KN_P4_UNFUSED) && !knob(KN_P4_BYTES) && !knob(KN_P4_NO_FLAT)) {
+        // 32-byte chunks from 3072-byte rows up: shorter rows put a row boundary in most
+        // warps' chunks, and the per-word fix-up pass is shorter over 4 words
+        // (32000x32002: 54.9 vs 57.7 us; 16000x16002: 18.1 vs 17.5; 8000x8001: 8.3 vs 7.1)
+        const bool c8 = al(p4_in, 32) && al(p4_out, 32) && !knob(KN_P4_FLAT16) &&
+                        (rb >= 3072 || knob(KN_P4_FLAT32));
+        const int cb = c8 ? 32 : 16;
         P4FlatParams fp;
         memset(&fp, 0, sizeof(fp));
         fp.in = p4_in; fp.out = p4_out;
-        fp.nbytes = (uint32_t)(n * h * rb);
+        fp.nbytes = (uint32_t)p4_bytes;
         fp.rb = (uint32_t)rb; fp.h = (uint32_t)h;
-        fp.nchunks = (fp.nbytes + 15) / 16;
+        fp.nchunks = (fp.nbytes + cb - 1) / cb;
         fp.wlast = (uint32_t)((w - 1) % 8);
         fp.fw = G.fillword;
         fp.s = (int)(rb % 4);
         fp.div_rb = make_fastdiv((uint32_t)rb);
         fp.div_h = make_fastdiv((uint32_t)h);
-        const unsigned grid = (fp.nchunks + 255) / 256;
-        switch ((int)((rb % 16) / 4)) {
-            case 0: launch_kb(p4_flat_kernel<0>, grid, 256u, 0, st, fp); break;
-            case 1: launch_kb(p4_flat_kernel<1>, grid, 256u, 0, st, fp); break;
-            case 2: launch_kb(p4_flat_kernel<2>, grid, 256u, 0, st, fp); break;
-            default: launch_kb(p4_flat_kernel<3>, grid, 256u, 0, st, fp); break;
+        const unsigned grid = (fp.nchunks + 247) / 248;        // 8 warps x 31 chunks
+        const int rdw = (int)((rb % cb) / 4);
+#define BE_K1P(CW, R, E) case R: launch_kb(p4_flat_kernel<CW, R, E>, grid, 256u, 0, st, fp); break;
+        // payloads under 4 MiB reload their edge chunks inline (4000x4001: 3.7 vs 4.2 us;
+        // 16000x16002: 18.8 vs 17.5 us)
+        if (c8) {
+            switch (rdw) { BE_K1P(8, 0, false) BE_K1P(8, 1, false) BE_K1P(8, 2, false) BE_K1P(8, 3, false)
+                           BE_K1P(8, 4, false) BE_K1P(8, 5, false) BE_K1P(8, 6, false) BE_K1P(8, 7, false) }
+        } else if (p4_bytes < ((int64_t)4 << 20)) {
+            switch (rdw) { BE_K1P(4, 0, true) BE_K1P(4, 1, true) BE_K1P(4, 2, true) BE_K1P(4, 3, true) }
+        } else {
+            switch (rdw) { BE_K1P(4, 0, false) BE_K1P(4, 1, false) BE_K1P(4, 2, false) BE_K1P(4, 3, false) }
         }
+#undef BE_K1P
         return cuda_check("p4_flat_kernel");
     }
     // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items cut

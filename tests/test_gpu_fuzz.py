@@ -177,3 +177,16 @@ def test_p4_flat_widths(w, cuda_dev, monkeypatch):
             ref = pbm.detect_p4(payload, n, h, w, fill).cpu().numpy().reshape(n, h, rb)
             monkeypatch.delenv("BITEDGE_P4_BYTES")
             assert (ref == out).all(), (n, h, w, fill)
+            # 16- / 32-byte chunks by knob, and 16 because a buffer is only 16-byte aligned
+            for kn in ("BITEDGE_P4_FLAT16", "BITEDGE_P4_FLAT32"):
+                monkeypatch.setenv(kn, "1")
+                ok = pbm.detect_p4(payload, n, h, w, fill).cpu().numpy().reshape(n, h, rb)
+                monkeypatch.delenv(kn)
+                assert (ref == ok).all(), (n, h, w, fill, kn)
+            nb = payload.numel()
+            src = torch.zeros(nb + 48, dtype=torch.uint8, device=cuda_dev)
+            dst = torch.full((nb + 48,), 0xA5, dtype=torch.uint8, device=cuda_dev)
+            src[16:16 + nb] = payload
+            pbm.detect_p4(src[16:16 + nb], n, h, w, fill, out=dst[16:16 + nb])
+            assert (dst[16:16 + nb].cpu().numpy().reshape(n, h, rb) == ref).all(), (n, h, w, fill, "+16")
+            assert (dst[:16] == 0xA5).all() and (dst[16 + nb:] == 0xA5).all(), (n, h, w, "guard")
