@@ -361,7 +361,7 @@ int try_flat(const void *in, uint32_t *o_edges, uint32_t *o_eset, const Geometry
     if (knob(KN_NO_FLAT)) return kNoKernel;
     const int64_t S = G.wp;                                    // uint32 words per row
     const int64_t nwords = nrows * S;
-    if (row_lo != 0 || row_hi != nrows || nwords >= ((int64_t)1 << 31) - 64 || S < 16 ||
+    if (row_lo != 0 || row_hi != nrows || nwords > ((int64_t)1 << 30) || S < 16 ||
         G.h >= ((int64_t)1 << 31))
         return kNoKernel;
     auto al = [](const void *p, int a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
@@ -379,7 +379,8 @@ int try_flat(const void *in, uint32_t *o_edges, uint32_t *o_eset, const Geometry
     fp.div_s = make_fastdiv((uint32_t)S);
     fp.div_h = make_fastdiv((uint32_t)G.h);
     const int ru = (int)((cw - S % cw) % cw);
-    const unsigned grid = (fp.nchunks + kThreads - 1) / kThreads;
+    constexpr unsigned per_cta = (kThreads / 32) * 31;        // a warp owns 31 chunks
+    const unsigned grid = (fp.nchunks + per_cta - 1) / per_cta;
     const int out = (o_edges && o_eset) ? kOutAny : o_eset ? kOutEset : kOutEdges;
 #define BE_FLAT_OUT(CWV, SW)                                                               \
     return out == kOutAny ? launch_flat_cw<CWV, SW, kOutAny>(fp, ru, grid, st)             \

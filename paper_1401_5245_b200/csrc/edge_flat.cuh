@@ -67,71 +67,69 @@ __device__ __forceinline__ void flat_load(const uint32_t *p, uint32_t (&v)[CW]) 
 }
 
 // SWAP: uint64 words (pixel word p at uint32 index p ^ 1); chunks hold whole pairs.
+//
+// A warp owns 31 consecutive chunks; lane 31 holds the chunk after them (the next
+// warp's first) only to feed the shuffles, so no lane reloads a neighbour's chunks and
+// every load of the thread is issued before the first wait.  Every word is first
+// evaluated as a word inside its row, inside its image (2 funnel shifts + 2 logic
+// ops); only chunks holding column 0, the last pixel word or padding words redo those
+// words with the row structure, and chunks in an image's first row or last two rows
+// redo all of theirs -- before this split every word paid for the row tests (43
+// thread instructions per word at 8192x8000 against the aligned K1's 21).
+#ifndef K1F_MINB
+#define K1F_MINB 5
+#endif
 template <int CW, int SWAP, int RU, int OUT>
-__global__ void __launch_bounds__(kThreads)
-edge_flat_kernel(const FlatParams p) {
+__global__ void __launch_bounds__(kThreads, CW == 8 ? (OUT == kOutAny ? 4 : K1F_MINB) : 0)
+edge_flat_kernel(const __grid_constant__ FlatParams p) {
     static_assert(RU > 0 && RU < CW && (!SWAP || RU % 2 == 0), "phase");
     constexpr int RD = CW - RU;                       // S mod CW
+    constexpr int LCW = CW == 8 ? 3 : 2;
     pdl_wait();
     pdl_trigger();
-    const uint32_t t = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const bool live = t < p.nchunks;
-    const uint32_t q = live ? t : p.nchunks - 1;      // dead lanes mirror the last chunk
-    const uint32_t base = q * CW;
-    const uint32_t S = p.S;
-    const uint32_t full = p.nwords / CW;              // chunks entirely inside the buffer
-    auto chunk_at = [&](int64_t w0) -> const uint32_t * {   // clamped aligned chunk
-        int64_t c = w0 / CW;
-        c = c < 0 ? 0 : (c >= full ? full - 1 : c);
-        return p.in + c * CW;
+    const uint32_t t = (blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * 31 + lane;
+    const bool live = lane < 31 && t < p.nchunks;
+    const uint32_t q = t < p.nchunks ? t : p.nchunks - 1;   // dead lanes mirror the last chunk
+    const int base = (int)(q * CW);                   // nwords <= 2^30: 32-bit word offsets
+    const int S = (int)p.S, nw = (int)p.nwords;
+    const int full = nw >> LCW;                       // chunks entirely inside the buffer
+    auto chunk_at = [&](int w0, uint32_t (&v)[CW]) {  // clamped aligned chunk
+        const int c = min(max(w0 >> LCW, 0), full - 1);
+        flat_load<CW>(p.in + (size_t)c * CW, v);
     };
 
     // ---- loads: up (aligned part + next lane), centre, down (aligned part + next lane)
-    uint32_t u0[CW], cm[CW], d0[CW], un[CW], dn[CW];
-    const int64_t au = (int64_t)base - S - RU;        // multiple of CW
-    const int64_t ad = (int64_t)base + S - RD;
-    flat_load<CW>(chunk_at(au), u0);
-    flat_load<CW>(chunk_at(base), cm);
-    flat_load<CW>(chunk_at(ad), d0);
-    // lane 31's successor chunks (the next warp's lane 0)
-    if (lane == 31) {
-        flat_load<CW>(chunk_at(au + CW), un);
-        flat_load<CW>(chunk_at(ad + CW), dn);
-    }
-    uint32_t lwm = 0, rwm = 0;                        // memory words before / after the chunk
-    if (lane == 0 && base > 0) lwm = __ldg(p.in + base - 1);
-    if (lane == 31 && base + CW < p.nwords) rwm = __ldg(p.in + base + CW);
+    uint32_t u0[CW], cm[CW], d0[CW];
+    chunk_at(base - S - RU, u0);                      // multiples of CW
+    chunk_at(base, cm);
+    chunk_at(base + S - RD, d0);
+    // the pixel word before the warp's chunks: memory word base-1 (u32) / base-2 (u64 pair)
+    uint32_t lwm = 0u;
+    if (lane == 0 && base >= 1 + SWAP) lwm = __ldg(p.in + base - 1 - SWAP);
 
     // up[j] = flat word base - S + j (memory order) = (u0 ++ next lane's u0)[RU + j]
     uint32_t up[CW], dw[CW];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
-        if (j + RU < CW) {
-            up[j] = u0[j + RU];
-        } else {
-            const uint32_t x = __shfl_down_sync(0xFFFFFFFFu, u0[j + RU - CW], 1);
-            up[j] = lane == 31 ? un[j + RU - CW] : x;
-        }
-        if (j + RD < CW) {
-            dw[j] = d0[j + RD];
-        } else {
-            const uint32_t x = __shfl_down_sync(0xFFFFFFFFu, d0[j + RD - CW], 1);
-            dw[j] = lane == 31 ? dn[j + RD - CW] : x;
-        }
+        if (j + RU < CW) up[j] = u0[j + RU];
+        else up[j] = __shfl_down_sync(0xFFFFFFFFu, u0[j + RU - CW], 1);
+        if (j + RD < CW) dw[j] = d0[j + RD];
+        else dw[j] = __shfl_down_sync(0xFFFFFFFFu, d0[j + RD - CW], 1);
     }
 
     // ---- chunks whose clamped vector loads may not cover what they need: the first
-    // and last two rows' worth of chunks and the ragged tail -- reload word by word
-    const bool edge_zone = base < S + 2 * CW || base + S + 2 * CW > p.nwords ||
-                           base + CW > p.nwords;
+    // and last two rows' worth of chunks and the ragged tail -- reload word by word,
+    // all loads in flight at once (an out-of-line word loop left the main path 1.5 %
+    // faster at 32768x32000 and the slowest warp, hence a 16 MB raster, 25 % slower)
+    const bool edge_zone = base < S + 2 * CW || base + S + 2 * CW > nw || base + CW > nw;
     if (edge_zone) {
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-            const int64_t f = (int64_t)base + j;
-            cm[j] = f < p.nwords ? __ldg(p.in + f) : 0u;
-            up[j] = f - S >= 0 && f - S < p.nwords ? __ldg(p.in + f - S) : 0u;
-            dw[j] = f + S < p.nwords ? __ldg(p.in + f + S) : 0u;
+            const int f = base + j;
+            cm[j] = f < nw ? __ldg(p.in + f) : 0u;
+            up[j] = f - S >= 0 && f - S < nw ? __ldg(p.in + f - S) : 0u;
+            dw[j] = f + S < nw ? __ldg(p.in + f + S) : 0u;
         }
     }
 
@@ -146,31 +144,39 @@ edge_flat_kernel(const FlatParams p) {
     // pixel-order word before the chunk: lane-1's last; after: lane+1's first
     uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cc[CW - 1], 1);
     uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
-    if (lane == 0) {
-        // pixel word base-1 is memory word base-1 (u32) or base-2 (u64 pair)
-        lw = SWAP ? (base >= 2 ? __ldg(p.in + base - 2) : 0u) : lwm;
-    }
-    if (lane == 31) {
-        rw = SWAP ? (base + CW + 1 < p.nwords ? __ldg(p.in + base + CW + 1) : 0u) : rwm;
-    }
+    if (lane == 0) lw = lwm;
     if (!live) return;
+    if (edge_zone && base + CW >= nw) rw = 0u;        // the buffer's last chunk: nothing after it
 
-    // ---- row / column of the chunk's first word; words past the row end wrap
-    const uint32_t r0 = fdiv(base, p.div_s);
-    const uint32_t c0 = base - r0 * S;
-    const uint32_t y0 = r0 - fdiv(r0, p.div_h) * p.h;
-    const uint32_t fw = p.fillword;
+    // ---- every word as a word inside its row, inside its image
     uint32_t ve[CW], vs[CW];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
+        const uint32_t left = j == 0 ? lw : cc[j - 1];
+        const uint32_t right = j == CW - 1 ? rw : cc[j + 1];
+        const uint32_t a = __funnelshift_r(cc[j], left, 1) | __funnelshift_l(right, cc[j], 1) |
+                           cu[j] | cd[j];
+        ve[j ^ SWAP] = cc[j] | ~a;
+        vs[j ^ SWAP] = ~cc[j] & a;
+    }
+
+    // ---- row / column of the chunk's first word; words past the row end wrap
+    const uint32_t r0 = fdiv((uint32_t)base, p.div_s);
+    const uint32_t c0 = (uint32_t)base - r0 * p.S;
+    const uint32_t y0 = r0 - fdiv(r0, p.div_h) * p.h;
+    const uint32_t fw = p.fillword;
+    // word j with its row structure: column 0 takes the left fill, the word holding
+    // pixel w-1 the right fill and the padding force, pure padding words are forced to
+    // 1, the first / last row of every image take the vertical fill
+    auto word = [&](int j) {
         uint32_t c = c0 + j, y = y0;
-        if (c >= S) {                                 // S >= 2 * CW: at most one wrap
-            c -= S;
+        if (c >= p.S) {                               // S >= 2 * CW: at most one wrap
+            c -= p.S;
             y = (y0 + 1 == p.h) ? 0 : y0 + 1;
         }
         const uint32_t left = j == 0 ? lw : cc[j - 1];
         const uint32_t right = j == CW - 1 ? rw : cc[j + 1];
-        uint32_t ln = __funnelshift_r(cc[j], c == 0 ? fw : left, 1);
+        const uint32_t ln = __funnelshift_r(cc[j], c == 0 ? fw : left, 1);
         uint32_t rn = __funnelshift_l(right, cc[j], 1);
         const uint32_t u = y == 0 ? fw : cu[j];
         const uint32_t d = y == p.h - 1 ? fw : cd[j];
@@ -184,14 +190,25 @@ edge_flat_kernel(const FlatParams p) {
         const uint32_t a = ln | rn | u | d;
         ve[j ^ SWAP] = cc[j] | ~a | f;
         vs[j ^ SWAP] = (~cc[j] & a) | f;
+    };
+    if (y0 == 0 || y0 + 2 >= p.h) {
+        // first row / last two rows of an image (a chunk may run on into the next row)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) word(j);
+    } else if (c0 == 0 || (int)(c0 + CW) > p.pl) {
+        // column 0 at word 0, or the row's last pixel word .. the next row's column 0
+        const int jlo = p.pl - (int)c0, jhi = S - (int)c0;
+#pragma unroll
+        for (int j = 0; j < CW; ++j)
+            if ((j == 0 && c0 == 0) || (j >= jlo && j <= jhi)) word(j);
     }
-    if (base + CW <= p.nwords) {
+    if (base + CW <= nw) {
         if (OUT != kOutEset) store_chunk<CW>(p.o_edges + base, ve);
         if (OUT != kOutEdges) store_chunk<CW>(p.o_eset + base, vs);
     } else {
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-            if (base + j < p.nwords) {
+            if (base + j < nw) {
                 if (OUT != kOutEset) p.o_edges[base + j] = ve[j];
                 if (OUT != kOutEdges) p.o_eset[base + j] = vs[j];
             }
