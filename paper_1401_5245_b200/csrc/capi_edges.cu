@@ -189,12 +189,42 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 
 // Returns kNoKernel when the register-direct kernel does not apply (caller falls back).
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
+// aligned uint8 rasters take K2t2 from this many row segments (rows x 2048-px segments)
+constexpr int64_t kTma2MinSegs = 12000;
 
-// K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA).
+// K2t2 strip height for the 0/1 pack, from the launch's row segments T = rows x
+// 2048-px segments (= warps x strip height).  Many waves of resident warps (24 per
+// SM): 8 rows, the tail is short.  A few waves: the rows are cut into strips that
+// fill a whole number of waves (8192^2: 4096 warps of 8-row strips are 1.15 waves of
+// 3552 -- 11.3 us, 19.5 serial; 820 strips of 10 rows x 4 segments are 0.92 -- 10.9
+// / 17.8 us).  Less than a wave of 8-row strips: shorter strips keep more copies in
+// flight (5000x5008: 5 rows 5.7 / 11.6 us, 8 rows 8.5 / 18.1, K2 8.7 / 12.1;
+// 6000x8000: 6 rows 11.9 / 15.8, 8 rows 11.5 / 18.3) -- `short_ok`: aligned rows of
+// whole 2048-px segments only (4096x4100 through the UNAL ring: 5.4 us at 5 rows,
+// 4.7 at 8).  scripts/u8_mid_sweep.py; BITEDGE_TMA2_RSL forces a height.
+inline int tma2_strip_rows(int64_t rows, int64_t nseg, bool short_ok) {
+    if (const char *v = knob(KN_TMA2_RSL)) {
+        const int r = atoi(v);
+        if (r >= 2 && r <= 4096) return r;
+    }
+    const int64_t cap = (int64_t)sm_count() * 24;
+    const int64_t T = rows * nseg, w8 = (rows + 7) / 8 * nseg;
+    if (w8 >= 8 * cap) return 8;
+    if (w8 <= cap) return (!short_ok || T < kTma2MinSegs) ? 8 : (T < 20000 ? 5 : 6);
+    const int64_t nw = w8 / cap;                         // whole waves at >= 8 rows per strip
+    const int64_t max_strips = nw * cap / nseg;
+    if (max_strips < 1) return 8;
+    const int64_t r = (rows + max_strips - 1) / max_strips;
+    return r < 8 ? 8 : (r > 64 ? 64 : (int)r);
+}
+
+// K2t2 launch for strip height RSL (4-slot rings, 8 warps per CTA); RSL = 0: the
+// run-time strip height rp.rsl.
 template <int RSL, bool UNAL = false>
 int launch_tma2(RegParams &rp, bool multi, bool halo, int64_t nseg, cudaStream_t st) {
     constexpr int kD = 4;
-    const int64_t nstrips = (rows_total(rp.row_lo, rp.row_hi) + RSL - 1) / RSL;
+    const int rsl = RSL > 0 ? RSL : rp.rsl;
+    const int64_t nstrips = (rows_total(rp.row_lo, rp.row_hi) + rsl - 1) / rsl;
     const int64_t nwarps = nstrips * nseg;
     const unsigned grid = (unsigned)((nwarps + 7) / 8);
     // ring slot: 16 + 2048 + 16 bytes (+32 for UNAL: granule-aligned copies)
@@ -250,8 +280,10 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
         if ((nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) && !knob(KN_TMA2_RSL32);
             const bool multi = o_packed != nullptr;
-            return short_strips ? launch_tma2<8, true>(rp, multi, false, nseg, st)
-                                : launch_tma2<32, true>(rp, multi, false, nseg, st);
+            if (!short_strips) return launch_tma2<32, true>(rp, multi, false, nseg, st);
+            rp.rsl = tma2_strip_rows(row_hi - row_lo, nseg, false);
+            return rp.rsl == 8 ? launch_tma2<8, true>(rp, multi, false, nseg, st)
+                               : launch_tma2<0, true>(rp, multi, false, nseg, st);
         }
     }
     {   // alignment of every row start (base and row stride)
@@ -580,21 +612,35 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
         const bool force = knob(KN_FORCE_TMA) != nullptr || (u64_out && knob(KN_U64_TMA));
-        if ((force || nwarps32 >= (int64_t)sm_count() * 24) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
-            // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
-            // strips, so the last wave's tail is a quarter as long: C5 737 ->
-            // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
-            // where the 25 % extra staged halo rows of 8-row strips cost more
-            // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
-            const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) &&
-                                      !knob(KN_TMA2_RSL32);
+        // Strip height: 8 rows for the 0/1 fast pack (4x the warps of 32-row
+        // strips, so the last wave's tail is a quarter as long: C5 737 ->
+        // 676 us); 32 rows when the pack is ALU-bound (threshold compare),
+        // where the 25 % extra staged halo rows of 8-row strips cost more
+        // than the tail (F2 on C5: 800 vs 921 us).  Sweep in DESIGN.md.
+        const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) && !knob(KN_TMA2_RSL32);
+        // Enough work to keep the ring kernels' copies in flight on every SM: 24 warps
+        // per SM of 32-row strips; with the 0/1 pack's short strips, 12 000 row
+        // segments (a 5000x5008 raster: 5.7 us against K2's 8.7; 8192^2: 10.9 vs 18.9 us,
+        // 1.06 vs 0.61 of the copy peak; 4096^2 stays with K2: 4.8 us either way)
+        int64_t min_segs = kTma2MinSegs;
+        if (const char *v = knob(KN_TMA2_MIN)) min_segs = atoll(v);
+        // (rows under 2048 px -- uint64 words from 1024 px -- half-fill their segments:
+        // 16x1024^2 is 6.8 us here against K2's 3.6)
+        const bool enough = (short_strips && G.w >= 2048)
+                                ? rows_total(row_lo, row_hi) * nseg >= min_segs
+                                : nwarps32 >= (int64_t)sm_count() * 24;
+        if ((force || enough) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool halo = above || below;
-            return short_strips ? launch_tma2<8>(rp, multi, halo, nseg, st)
-                                : launch_tma2<32>(rp, multi, halo, nseg, st);
+            if (!short_strips) return launch_tma2<32>(rp, multi, halo, nseg, st);
+            rp.rsl = tma2_strip_rows(rows_total(row_lo, row_hi), nseg, G.w >= 2048);
+            return rp.rsl == 8 ? launch_tma2<8>(rp, multi, halo, nseg, st)
+                               : launch_tma2<0>(rp, multi, halo, nseg, st);
         }
     }
     if (!k2_outs && input_kind == 1) return kNoKernel;   // other uint8 multi-output: tile kernel
     if (input_kind == 1 && !u64_out && !o_packed && G.w >= 1024 && !knob(KN_NO_TMA)) {
+        // (8-row strips, as in K2t2, measured slower here at every size: 4096^2 8.3 us
+        // against K2's 4.8, 8192^2 24.1 against K2t2's 11.1)
         constexpr int kRSLT = 32, kD = 6;
         const int64_t nseg = (G.w + 1023) / 1024;
         const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;

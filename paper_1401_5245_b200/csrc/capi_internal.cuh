@@ -59,6 +59,8 @@ enum Knob : int {
     KN_P4_FLAT16,
     KN_P4_FLAT_MAX,
     KN_P4_FLAT32,
+    KN_TMA2_MIN,
+    KN_TMA2_RSL,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

@@ -54,6 +54,7 @@ struct RegParams {
     const char *in_end;      // K1 UNAL: end of the input buffer (loads stop there)
     int unal_words;          // K1 UNAL: load the 4 words one by one instead of 2 chunks
     int h16;                 // K1: 8-word items from 16-byte (not 32-byte) aligned rows
+    int rsl;                 // K2t2 with RSL = 0: rows per strip (>= 2)
 };
 
 // kOutAll: every requested output of one word from the values the edge formula
@@ -1040,7 +1041,10 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     if (gw >= nwarps) return;
     const int64_t strip = gw / nseg;
     const int seg = (int)(gw - strip * nseg);
-    const int64_t g0 = p.row_lo + strip * RSL;
+    // strip height: the template constant, or (RSL == 0) the launch's p.rsl -- the host
+    // fits mid-size rasters into whole waves of resident warps with it
+    const int rsl = RSL > 0 ? RSL : p.rsl;
+    const int64_t g0 = p.row_lo + strip * rsl;
     const int64_t x0 = (int64_t)seg * SEG;
     const int ca = seg * 64 + lane, cb = ca + 32;    // this lane's two output words
     // their uint32 store columns: uint64 output stores pixel word c at c ^ 1
@@ -1053,8 +1057,7 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
     const int64_t b_hi = x0 + SEG + 16 < wr ? x0 + SEG + 16 : wr;
     const uint32_t seg_bytes = (uint32_t)(b_hi - b_lo);
     const int dst_off = (int)(b_lo - (x0 - 16));
-    constexpr int NST = RSL + 2;
-    static_assert(RSL >= 2, "fetch order needs two own rows");
+    const int NST = rsl + 2;                         // rsl >= 2: the fetch order needs two own rows
     // staged rows i in [i_lo, i_hi) lie inside `in`; row 0 / row lim may be halos
     const int i_lo = g0 == 0 ? 1 : 0;
     const int64_t lim = p.nrows - (g0 - 1);
@@ -1206,7 +1209,7 @@ edge_tma2_u8_kernel(const RegParams p, int64_t nseg, int64_t nwarps) {
         if (++y == p.h) y = 0;
         ua = xa; ub = xb; xa = na; xb = nb; el = nel; er = ner;
     }
-    emit(RSL - 1, y, ua, ub, xa, xb, dwa, dwb, el, er);
+    emit(rsl - 1, y, ua, ub, xa, xb, dwa, dwb, el, er);
     uint32_t upa, upb;                                // above halo (staged 0)
     fetch(NST - 1, upa, upb, t0, t1);
     emit(0, y0, upa, upb, c0a, c0b, c1a, c1b, el0, er0);

@@ -12,26 +12,8 @@ from paper_1401_5245_b200 import cuda as cu  # noqa: E402
 dev = torch.device("cuda:0")
 
 
-def timed(step, k, nstreams):
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        cur = torch.cuda.current_stream()
-        side = [torch.cuda.Stream() for _ in range(nstreams)]
-        for s_ in side:
-            s_.wait_stream(cur)
-        for i in range(k):
-            with torch.cuda.stream(side[i % nstreams]):
-                step(i)
-        for s_ in side:
-            cur.wait_stream(s_)
-    g.replay()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    g.replay()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) * 1e3 / k
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from u8_widths_lib import timed  # noqa: E402
 
 
 for (n, h, w) in ((1, 16384, 16384), (1, 16384, 16100), (1, 16384, 16001), (1, 4096, 4096), (1, 4096, 4100), (1, 4096, 4000), (16, 1024, 1024), (16, 1024, 1000),

@@ -17,7 +17,7 @@ KNOBS = [{}, {"BITEDGE_KERNEL": "tile"}, {"BITEDGE_KERNEL": "stream"}, {"BITEDGE
          {"BITEDGE_NO_ROLL": "1"}, {"BITEDGE_NO_WARPIMG": "1"}, {"BITEDGE_FORCE_TMA": "1"},
          {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA1": "1"}, {"BITEDGE_PDL": "0"},
          {"BITEDGE_RS": "8"}, {"BITEDGE_WARPIMG_G4": "1"}, {"BITEDGE_PDL_LATE": "1"},
-         {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"}, {"BITEDGE_K1_GENERIC": "1"}, {"BITEDGE_NO_UNAL": "1"}, {"BITEDGE_UNAL_CHUNKS": "1"}, {"BITEDGE_UNAL_BYTES": "1"}, {"BITEDGE_U64_TMA": "1"}]
+         {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"}, {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "5"}, {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "11"}, {"BITEDGE_K1_GENERIC": "1"}, {"BITEDGE_NO_UNAL": "1"}, {"BITEDGE_UNAL_CHUNKS": "1"}, {"BITEDGE_UNAL_BYTES": "1"}, {"BITEDGE_U64_TMA": "1"}]
 
 
 def _shape(rng):

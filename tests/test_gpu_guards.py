@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 KNOBS = [{}, {"BITEDGE_KERNEL": "tile"}, {"BITEDGE_KERNEL": "stream"}, {"BITEDGE_CW4": "1"},
          {"BITEDGE_NO_ROLL": "1"}, {"BITEDGE_NO_WARPIMG": "1"}, {"BITEDGE_FORCE_TMA": "1"},
          {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA1": "1"}, {"BITEDGE_RS": "8"},
-         {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"}, {"BITEDGE_K1_GENERIC": "1"}, {"BITEDGE_NO_UNAL": "1"}, {"BITEDGE_NO_TMA": "1"}]
+         {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"}, {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "5"}, {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "11"}, {"BITEDGE_K1_GENERIC": "1"}, {"BITEDGE_NO_UNAL": "1"}, {"BITEDGE_NO_TMA": "1"}]
 SHAPES = [(3, 64, 64), (1, 37, 2048), (2, 19, 1000), (1, 5, 4096), (4, 9, 33), (1, 70, 3000)]
 SENT = 0x5A5A5A5A
 GUARD = 96                                   # words before and after each output view

@@ -30,12 +30,15 @@ def _view(torch, dev, a, base_off, pad):
 
 @pytest.mark.parametrize("w", [2049, 2050, 2063, 4100, 6001, 8191])
 @pytest.mark.parametrize("base_off,pad", [(0, 0), (1, 0), (7, 3), (13, 0), (4, 12)])
-def test_unal_tma_forced(cuda_dev, monkeypatch, w, base_off, pad):
+@pytest.mark.parametrize("rsl", [None, "5"])
+def test_unal_tma_forced(cuda_dev, monkeypatch, w, base_off, pad, rsl):
     import torch
 
     from paper_1401_5245_b200 import cuda as cu
 
     monkeypatch.setenv("BITEDGE_FORCE_TMA", "1")
+    if rsl:
+        monkeypatch.setenv("BITEDGE_TMA2_RSL", rsl)   # run-time strip height
     rng = np.random.default_rng(w + 17 * base_off + pad)
     n, h = 2, 19
     a = (rng.random((n, h, w)) < 0.55).astype(np.uint8) * rng.integers(1, 256, (n, h, w),

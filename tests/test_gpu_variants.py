@@ -34,6 +34,9 @@ VARIANTS = {
     "warpimg_g4": {"BITEDGE_WARPIMG_G4": "1"},
     "pdl_late": {"BITEDGE_PDL_LATE": "1"},
     "tma_warp_rsl32": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL32": "1"},
+    "tma_warp_rsl3": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "3"},
+    "tma_warp_rsl6": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "6"},
+    "tma_warp_rsl13": {"BITEDGE_FORCE_TMA": "1", "BITEDGE_TMA2_RSL": "13"},
     "k1_generic": {"BITEDGE_K1_GENERIC": "1"},
     "k1_prs2": {"BITEDGE_PRS": "2"},
     "k1_prs8": {"BITEDGE_PRS": "8"},
