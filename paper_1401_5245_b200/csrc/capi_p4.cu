@@ -517,8 +517,40 @@ extern "C" int be_p4_edges(const uint8_t *p4_in, uint8_t *p4_out, int64_t n, int
 #undef BE_K1P
         return cuda_check("p4_flat_kernel");
     }
-    // rows of whole 4-byte words (w % 32 == 0 or 25..31): K1 with 4-word items cut
-    // out of aligned 16-byte chunks (UNAL)
+    // rows of whole 4-byte words (w % 32 == 0 or 25..31) that are not a multiple of the
+    // vector width: K1f's flat view with the P4 conversions (edge_flat.cuh)
+    if (rb % 4 == 0 && !knob(KN_P4_UNFUSED) && !knob(KN_P4_BYTES) && !knob(KN_NO_FLAT) &&
+        !knob(KN_P4_NO_FLAT)) {
+        const int64_t S = rb / 4, nwords = n * h * S;
+        const int cw = (al(p4_in, 32) && al(p4_out, 32)) ? 8 : (al(p4_in, 16) && al(p4_out, 16)) ? 4 : 0;
+        if (cw != 0 && S >= 16 && S % cw != 0 && nwords <= ((int64_t)1 << 30) &&
+            h < ((int64_t)1 << 31)) {
+            FlatParams fp;
+            memset(&fp, 0, sizeof(fp));
+            fp.in = (const uint32_t *)p4_in;
+            fp.o_edges = (uint32_t *)p4_out;
+            fp.nwords = (uint32_t)nwords; fp.S = (uint32_t)S; fp.h = (uint32_t)h;
+            fp.nrows = (uint32_t)(n * h);
+            fp.pl = G.pl; fp.lastbit = G.lastbit; fp.padmask = G.padmask; fp.fillword = G.fillword;
+            fp.nchunks = (uint32_t)((nwords + cw - 1) / cw);
+            fp.div_s = make_fastdiv((uint32_t)S);
+            fp.div_h = make_fastdiv((uint32_t)h);
+            const int ru = (int)((cw - S % cw) % cw);
+            constexpr unsigned per_cta = (kThreads / 32) * 31;    // a warp owns 31 chunks
+            const unsigned grid = (fp.nchunks + per_cta - 1) / per_cta;
+#define BE_K1F_P4(CW, R) case R: launch_k(edge_flat_kernel<CW, 0, R, kOutEdges, true>, grid, 0, st, fp); break;
+            if (cw == 8) {
+                switch (ru) { BE_K1F_P4(8, 1) BE_K1F_P4(8, 2) BE_K1F_P4(8, 3) BE_K1F_P4(8, 4)
+                              BE_K1F_P4(8, 5) BE_K1F_P4(8, 6) BE_K1F_P4(8, 7) }
+            } else {
+                switch (ru) { BE_K1F_P4(4, 1) BE_K1F_P4(4, 2) BE_K1F_P4(4, 3) }
+            }
+#undef BE_K1F_P4
+            return cuda_check("edge_flat_kernel<P4>");
+        }
+    }
+    // other rows of whole 4-byte words: K1 with 4-word items cut out of aligned 16-byte
+    // chunks (UNAL)
     if (rb % 4 == 0 && al(p4_in, 4) && al(p4_out, 4) && !knob(KN_P4_UNFUSED) &&
         !knob(KN_P4_BYTES) && n * h < ((int64_t)1 << 31)) {
         RegParams rp;

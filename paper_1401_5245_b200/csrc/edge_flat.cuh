@@ -79,10 +79,17 @@ __device__ __forceinline__ void flat_load(const uint32_t *p, uint32_t (&v)[CW]) 
 #ifndef K1F_MINB
 #define K1F_MINB 5
 #endif
-template <int CW, int SWAP, int RU, int OUT>
+//
+// P4: the words are PBM P4 payload bytes (rows of whole 4-byte words; 1 = black,
+// MSB-first bytes: the byte-reversed, inverted pixel-order word).  The plain path
+// stays in the P4 domain as K1's P4 variant does -- only the two horizontal shifts
+// run in pixel order: out = c & ~(pi(L & R) & u & d) -- and the row-structure words
+// convert to the white pixel-order domain and back.
+template <int CW, int SWAP, int RU, int OUT, bool P4 = false>
 __global__ void __launch_bounds__(kThreads, CW == 8 ? (OUT == kOutAny ? 4 : K1F_MINB) : 0)
 edge_flat_kernel(const __grid_constant__ FlatParams p) {
     static_assert(RU > 0 && RU < CW && (!SWAP || RU % 2 == 0), "phase");
+    static_assert(!P4 || (SWAP == 0 && OUT == kOutEdges), "P4: uint32 rows, edges only");
     constexpr int RD = CW - RU;                       // S mod CW
     constexpr int LCW = CW == 8 ? 3 : 2;
     pdl_wait();
@@ -137,14 +144,14 @@ edge_flat_kernel(const __grid_constant__ FlatParams p) {
     uint32_t cc[CW], cu[CW], cd[CW];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
-        cc[j] = cm[j ^ SWAP];
-        cu[j] = up[j ^ SWAP];
+        cc[j] = P4 ? p4_pi(cm[j]) : cm[j ^ SWAP];     // P4: pixel order, 1 = black
+        cu[j] = up[j ^ SWAP];                         // P4: as loaded
         cd[j] = dw[j ^ SWAP];
     }
     // pixel-order word before the chunk: lane-1's last; after: lane+1's first
     uint32_t lw = __shfl_up_sync(0xFFFFFFFFu, cc[CW - 1], 1);
     uint32_t rw = __shfl_down_sync(0xFFFFFFFFu, cc[0], 1);
-    if (lane == 0) lw = lwm;
+    if (lane == 0) lw = P4 ? p4_pi(lwm) : lwm;
     if (!live) return;
     if (edge_zone && base + CW >= nw) rw = 0u;        // the buffer's last chunk: nothing after it
 
@@ -154,6 +161,12 @@ edge_flat_kernel(const __grid_constant__ FlatParams p) {
     for (int j = 0; j < CW; ++j) {
         const uint32_t left = j == 0 ? lw : cc[j - 1];
         const uint32_t right = j == CW - 1 ? rw : cc[j + 1];
+        if (P4) {
+            const uint32_t lr = __funnelshift_r(cc[j], left, 1) & __funnelshift_l(right, cc[j], 1);
+            ve[j] = cm[j] & ~(p4_pi(lr) & cu[j] & cd[j]);
+            vs[j] = 0u;
+            continue;
+        }
         const uint32_t a = __funnelshift_r(cc[j], left, 1) | __funnelshift_l(right, cc[j], 1) |
                            cu[j] | cd[j];
         ve[j ^ SWAP] = cc[j] | ~a;
@@ -174,12 +187,14 @@ edge_flat_kernel(const __grid_constant__ FlatParams p) {
             c -= p.S;
             y = (y0 + 1 == p.h) ? 0 : y0 + 1;
         }
-        const uint32_t left = j == 0 ? lw : cc[j - 1];
-        const uint32_t right = j == CW - 1 ? rw : cc[j + 1];
-        const uint32_t ln = __funnelshift_r(cc[j], c == 0 ? fw : left, 1);
-        uint32_t rn = __funnelshift_l(right, cc[j], 1);
-        const uint32_t u = y == 0 ? fw : cu[j];
-        const uint32_t d = y == p.h - 1 ? fw : cd[j];
+        // white pixel-order domain (P4: centre / neighbours inverted, up / down converted)
+        const uint32_t cw = P4 ? ~cc[j] : cc[j];
+        const uint32_t left = P4 ? ~(j == 0 ? lw : cc[j - 1]) : (j == 0 ? lw : cc[j - 1]);
+        const uint32_t right = P4 ? ~(j == CW - 1 ? rw : cc[j + 1]) : (j == CW - 1 ? rw : cc[j + 1]);
+        const uint32_t ln = __funnelshift_r(cw, c == 0 ? fw : left, 1);
+        uint32_t rn = __funnelshift_l(right, cw, 1);
+        const uint32_t u = y == 0 ? fw : (P4 ? ~p4_pi(cu[j]) : cu[j]);
+        const uint32_t d = y == p.h - 1 ? fw : (P4 ? ~p4_pi(cd[j]) : cd[j]);
         uint32_t f = 0u;
         if ((int)c == p.pl) {
             rn = (rn & ~p.lastbit) | (fw & p.lastbit);
@@ -188,8 +203,8 @@ edge_flat_kernel(const __grid_constant__ FlatParams p) {
             f = 0xFFFFFFFFu;
         }
         const uint32_t a = ln | rn | u | d;
-        ve[j ^ SWAP] = cc[j] | ~a | f;
-        vs[j ^ SWAP] = (~cc[j] & a) | f;
+        ve[j ^ SWAP] = P4 ? p4_pi(~(cw | ~a | f)) : (cw | ~a | f);   // P4: 1 = black, padding 0
+        vs[j ^ SWAP] = (~cw & a) | f;
     };
     if (y0 == 0 || y0 + 2 >= p.h) {
         // first row / last two rows of an image (a chunk may run on into the next row)

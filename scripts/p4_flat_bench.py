@@ -11,10 +11,10 @@ from paper_1401_5245_b200 import _capi  # noqa: E402
 from paper_1401_5245_b200 import pbm  # noqa: E402
 
 dev = torch.device("cuda:0")
-MODES = (("default", {}), ("K1p 32 B", {"BITEDGE_P4_FLAT32": "1"}), ("K1p 16 B", {"BITEDGE_P4_FLAT16": "1"}), ("byte kernel", {"BITEDGE_P4_BYTES": "1"}))
+MODES = (("default", {}), ("K1p 32 B", {"BITEDGE_P4_FLAT32": "1"}), ("K1p 16 B", {"BITEDGE_P4_FLAT16": "1"}), ("no flat", {"BITEDGE_P4_NO_FLAT": "1"}), ("byte kernel", {"BITEDGE_P4_BYTES": "1"}))
 peak = 6540.0
 lines = []
-for (h, w) in ((32000, 32002), (32000, 31999), (16000, 16002), (12000, 12002), (8000, 8001),
+for (h, w) in ((32000, 32002), (32000, 31993), (8000, 8000), (8000, 7993), (16000, 16002), (12000, 12002), (8000, 8001),
                (4000, 4001), (2000, 2000), (1000, 1001), (256, 250)):
     rb = (w + 7) // 8
     nbytes = h * rb

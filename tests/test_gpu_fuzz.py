@@ -150,11 +150,13 @@ def test_fuzz_halo_slabs_all_inputs(knob, cuda_dev, monkeypatch):
 
 
 @pytest.mark.parametrize("w", [25, 31, 33, 57, 100, 127, 129, 250, 255, 257, 1000, 1001, 2047,
-                               4100, 8001, 32002])
+                               4100, 8001, 32002,
+                               539, 544, 1180, 1216, 8000, 31993, 32032])   # rows of whole words: K1f P4
 def test_p4_flat_widths(w, cuda_dev, monkeypatch):
     """K1p (P4 payloads viewed as one flat byte array) for every row-length
-    phase mod 16 bytes, batches whose images start mid-word, h = 1 / 2 / many,
-    both borders -- against the oracle and against the byte kernel."""
+    phase mod 16 bytes, and K1f's P4 variant for rows of whole 4-byte words that
+    are not vector multiples; batches whose images start mid-word, h = 1 / 2 /
+    many, both borders -- against the oracle and against the byte kernel."""
     import torch
 
     from paper_1401_5245_b200 import pbm
