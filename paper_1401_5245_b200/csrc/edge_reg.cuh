@@ -504,8 +504,15 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
 // 32-bit words around them (L1-cached loads) and one byte permute per word;
 // never read past `in_end`.  Output words go to column c ^ oswap (1: the
 // drop-in's uint64 layout; the u64 row's last u32 word may be pure padding).
+// Aligned 4-row strips at 64 registers (4 CTAs/SM; ~20 bytes of spills): a 4096^2
+// raster's 512 CTAs are one wave instead of 1.15 of the 74-register build's 444
+// (4.58 -> 4.36 us, 8.25 -> 6.38 us on one stream; 16x1024^2 6.31 -> 5.52 us).  The
+// UNAL variants were mixed (16x1024x1000: 8.7 -> 7.7 us serial, 3.97 -> 4.15 overlapped).
+#ifndef K2_MINB
+#define K2_MINB 4
+#endif
 template <int RS, int OUT, bool HALO, bool V8, int UNAL = 0>   // UNAL: 0, 1 (any byte), 4, 8 (row alignment)
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (RS == 4 && UNAL == 0 && OUT != kOutAny) ? K2_MINB : 0)
 edge_reg_u8_kernel(const RegParams p) {
     pdl_wait();
     pdl_trigger();
