@@ -14,6 +14,10 @@ for c in c1 c2 c3 c5; do
 done
 timeout -k 10 300 python scripts/k1_widths.py > gpurun_out/fin/k1w.log 2>&1
 timeout -k 10 300 python scripts/u8_widths.py > gpurun_out/fin/u8w.log 2>&1
+timeout -k 10 300 python scripts/u8_mid_sweep.py final > gpurun_out/fin/u8mid.log 2>&1
+K1W_SHAPES=6000x6016,10000x10016,12000x11968,12288x12288,16384x16000,16384x16384,24576x24576 timeout -k 10 300 python scripts/k1_widths.py > gpurun_out/fin/k1mid.log 2>&1
+timeout -k 10 300 python scripts/p4_flat_bench.py gpurun_out/fin/p4_flat.txt > gpurun_out/fin/p4_flat.log 2>&1
+timeout -k 10 300 python scripts/p4_ragged_bench.py > gpurun_out/fin/p4_ragged.log 2>&1
 timeout -k 10 300 python scripts/dropin_latency.py gpurun_out/fin/dropin.json > gpurun_out/fin/dropin.log 2>&1
 timeout -k 10 600 python scripts/bench_next.py gpurun_out/fin/bench_next.json > gpurun_out/fin/bench_next.log 2>&1
 TAG=r2 LAUNCH_CFG=c4 timeout -k 10 1800 bash scripts/gpu_profiles.sh > gpurun_out/fin/profiles.log 2>&1

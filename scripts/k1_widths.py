@@ -33,9 +33,12 @@ def timed(step, k, nstreams):
     return a.elapsed_time(b) * 1e3 / k
 
 
+SHAPES = ((8192, 8192), (8192, 8000), (8192, 8064), (8192, 8160), (8192, 7999),
+          (4096, 16384 - 32), (32768, 32000))
+if os.environ.get("K1W_SHAPES"):      # e.g. K1W_SHAPES=4096x4096,16384x16384
+    SHAPES = tuple(tuple(int(v) for v in t.split("x")) for t in os.environ["K1W_SHAPES"].split(","))
 for bits in (32, 64):
-    for (h, w) in ((8192, 8192), (8192, 8000), (8192, 8064), (8192, 8160), (8192, 7999),
-                   (4096, 16384 - 32), (32768, 32000)):
+    for (h, w) in SHAPES:
         wp = -(-w // bits)
         dt = torch.int32 if bits == 32 else torch.int64
         nbytes = h * wp * bits // 8

@@ -38,7 +38,11 @@ HOT = [  # (label, substring of the demangled name)
     ("K3 halo (C4 row shards)", "edge_reg_packed_kernel<0, 4, 8, 0, true, false, true, false, false>"),
     ("K3e end rows of a row shard", "edge_halo_ends_kernel"),
     ("K1 H16 (16-byte rows, 8-word items)", "edge_reg_packed_kernel<0, 2, 8, 0, false, false, false, false, true>"),
-    ("K1f flat (ragged packed rows)", "edge_flat_kernel<8, 0, 6, 0>"),
+    ("K1f flat (ragged packed rows)", "edge_flat_kernel<8, 0, 6, 0, false>"),
+    ("K1f flat, P4 rows of whole words", "edge_flat_kernel<8, 0, 6, 0, true>"),
+    ("K1p flat P4 bytes, 32-byte chunks", "p4_flat_kernel<8, 0, false>"),
+    ("K1p flat P4 bytes, 16-byte chunks", "p4_flat_kernel<4, 0, true>"),
+    ("K2t2 TMA ring, run-time strip height (mid-size uint8 rasters)", "edge_tma2_u8_kernel<0, 4, 0, false, false>"),
     ("K2w warp-per-image (C2 glyphs)", "edge_warp_img_kernel<1, 0, 8>"),
     ("K2t2 TMA ring (C5 pages)", "edge_tma2_u8_kernel<8, 4, 0, false, false>"),
     ("K2t2 UNAL (uint8 rows at byte offsets)", "edge_tma2_u8_kernel<8, 4, 0, false, true>"),

@@ -13,6 +13,8 @@ from u8_widths_lib import timed  # noqa: E402
 
 dev = torch.device("cuda:0")
 KNOBS = [{}, {"BITEDGE_NO_TMA": "1"}] + [{"BITEDGE_TMA2_MIN": "0", "BITEDGE_TMA2_RSL": str(r)} for r in (4, 5, 6, 8, 10, 12, 16, 24)]
+if len(sys.argv) > 1 and sys.argv[1] == "final":    # the dispatch as shipped against K2 alone
+    KNOBS = [{}, {"BITEDGE_NO_TMA": "1"}]
 for (n, h, w) in ((1, 4096, 4096), (4, 2048, 2048), (1, 3000, 5008), (1, 5000, 5008), (1, 6000, 6016), (1, 6000, 8000), (1, 8192, 8192),
                   (1, 12288, 12288), (1, 16384, 16384), (1, 8192, 8100)):
     nbytes = n * h * w
