@@ -191,6 +191,15 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 // aligned uint8 rasters take K2t2 from this many row segments (rows x 2048-px segments)
 constexpr int64_t kTma2MinSegs = 12000;
+// ... and from this row width: a 2048-px segment that is >= 62 % full still beats the
+// one-shot K2, whose warps straddle rows that are not 1024-px multiples (batches of
+// 1920x1080 frames: 35.6 -> 21.7 us, 0.64 -> 1.05 of the copy peak; 1600x1200: 21.0 ->
+// 14.2 us; 1280x1024: 16.1 -> 14.4 us; 1024-px rows stay with K2: 12.8 vs 19.7 us).
+// BITEDGE_TMA2_MINW overrides it.
+inline int64_t tma2_min_width() {
+    if (const char *v = knob(KN_TMA2_MINW)) return atoll(v);
+    return 1280;
+}
 
 // K2t2 strip height for the 0/1 pack, from the launch's row segments T = rows x
 // 2048-px segments (= warps x strip height).  Many waves of resident warps (24 per
@@ -272,12 +281,16 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     // rows >= 2048 px: the TMA ring (K2t2) with granule-aligned copies and a
     // per-row realignment of the packed words (16384 x 16100: 45 -> 95 % of the
     // copy peak); K2 UNAL below otherwise
-    if (G.w >= 2048 && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
+    if (G.w >= tma2_min_width() && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (row_hi - row_lo + 31) / 32 * nseg;
-        // (no minimum work, unlike aligned rows: at 4096 x 4100 the ring is 4.74 us
-        // against K2 UNAL's 6.46 us)
-        if ((nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
+        // (no minimum work from 2048 px, unlike aligned rows: at 4096 x 4100 the ring is
+        // 4.74 us against K2 UNAL's 6.46 us; narrower rows half-fill their segment and
+        // need the aligned rows' minimum: 8000 x 1500 is 5.45 us here, 5.01 in K2 UNAL,
+        // a batch of 64 1900 x 1080 frames 24.6 against 49.4 us)
+        const bool enough = G.w >= 2048 || (row_hi - row_lo) * nseg >= kTma2MinSegs ||
+                            knob(KN_FORCE_TMA);
+        if (enough && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool short_strips = (thr == 1 || knob(KN_TMA2_RSL8)) && !knob(KN_TMA2_RSL32);
             const bool multi = o_packed != nullptr;
             if (!short_strips) return launch_tma2<32, true>(rp, multi, false, nseg, st);
@@ -607,7 +620,8 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
-    if (input_kind == 1 && (G.w >= 2048 || (u64_out && !u64_k2)) && !knob(KN_NO_TMA) &&
+    const int64_t tma2_minw = tma2_min_width();
+    if (input_kind == 1 && (G.w >= tma2_minw || (u64_out && !u64_k2)) && !knob(KN_NO_TMA) &&
         (!knob(KN_TMA1) || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (rows_total(row_lo, row_hi) + 31) / 32 * nseg;
@@ -626,13 +640,13 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         if (const char *v = knob(KN_TMA2_MIN)) min_segs = atoll(v);
         // (rows under 2048 px -- uint64 words from 1024 px -- half-fill their segments:
         // 16x1024^2 is 6.8 us here against K2's 3.6)
-        const bool enough = (short_strips && G.w >= 2048)
+        const bool enough = (short_strips && G.w >= tma2_minw)
                                 ? rows_total(row_lo, row_hi) * nseg >= min_segs
                                 : nwarps32 >= (int64_t)sm_count() * 24;
         if ((force || enough) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool halo = above || below;
             if (!short_strips) return launch_tma2<32>(rp, multi, halo, nseg, st);
-            rp.rsl = tma2_strip_rows(rows_total(row_lo, row_hi), nseg, G.w >= 2048);
+            rp.rsl = tma2_strip_rows(rows_total(row_lo, row_hi), nseg, G.w >= tma2_minw);
             return rp.rsl == 8 ? launch_tma2<8>(rp, multi, halo, nseg, st)
                                : launch_tma2<0>(rp, multi, halo, nseg, st);
         }

@@ -61,6 +61,7 @@ enum Knob : int {
     KN_P4_FLAT32,
     KN_TMA2_MIN,
     KN_TMA2_RSL,
+    KN_TMA2_MINW,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];

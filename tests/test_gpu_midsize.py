@@ -25,7 +25,11 @@ def _pages(h, w, seed):
                                  (2900, 10240),     # 5 segments per row, 5-row strips
                                  (5200, 8192),      # 20 800 row segments: 6-row strips
                                  (8192, 8192),      # 1.15 waves of 8-row strips -> 10-row strips
-                                 (7000, 6148)])     # ragged rows through the UNAL ring
+                                 (7000, 6148),      # ragged rows through the UNAL ring
+                                 (12960, 1920),     # 12 frames of 1920 x 1080: one 94 %-full segment
+                                 (12000, 1600),     # 78 %-full segments
+                                 (12960, 1900),     # ragged 1900-px rows: UNAL ring under 2048 px
+                                 (16000, 1290)])    # 63 %-full ragged segments
 def test_u8_midsize_default_dispatch(cuda_dev, h, w):
     import torch
 
