@@ -614,11 +614,20 @@ edge_reg_u8_kernel(const RegParams p) {
                 }
             }
             if (i >= 1 && i <= RS) {
-                lbit[i - 1] = fw;
-                rbit[i - 1] = 0u;
-                if (ok && need_l) lbit[i - 1] = (uint8_t)ptr[-1] >= T.t ? 1u : 0u;
-                if (ok && need_r) rbit[i - 1] = (uint8_t)ptr[32] >= T.t ? 0x80000000u : 0u;
+                // the neighbour bytes across warps (lanes 0 / 31), raw: comparing them
+                // here made the warp wait for each byte before issuing the next row's
+                // loads (rows that are not 1024-px multiples; 256 x 480 x 640: ncu
+                // long-scoreboard 7.0 against 2.5 on 512-px rows)
+                lbit[i - 1] = 0xFFFFFFFFu;
+                rbit[i - 1] = 0xFFFFFFFFu;
+                if (ok && need_l) lbit[i - 1] = (uint8_t)ptr[-1];
+                if (ok && need_r) rbit[i - 1] = (uint8_t)ptr[32];
             }
+        }
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            lbit[r] = lbit[r] == 0xFFFFFFFFu ? fw : (lbit[r] >= (uint32_t)T.t ? 1u : 0u);
+            rbit[r] = rbit[r] == 0xFFFFFFFFu ? 0u : (rbit[r] >= (uint32_t)T.t ? 0x80000000u : 0u);
         }
 #pragma unroll
         for (int i = 0; i < RS + 2; ++i) wd[i] = pack32_any(ra[i], rb2[i], T);
@@ -693,7 +702,7 @@ edge_roll_u8_kernel(const RegParams p) {
     const int nvis = live ? (int)(lim < RSL + 2 ? lim : RSL + 2) : 0;   // rows i < nvis exist
     const char *safe = p.in + x0;
     uint4 ra[Q], rb2[Q];
-    uint32_t eb[Q];
+    uint32_t ebl[Q], ebr[Q];       // raw neighbour bytes across warps, compared at use (see K2)
     uint32_t okm = 0u;                                                 // bit slot: row present
     auto issue = [&](int i, int slot) {
         const char *ptr = base + i * rb;
@@ -704,9 +713,11 @@ edge_roll_u8_kernel(const RegParams p) {
         }
         ldg_stream_v8(ok ? ptr : safe, ra[slot], rb2[slot]);
         okm = ok ? (okm | (1u << slot)) : (okm & ~(1u << slot));
-        uint32_t e = ldg_u8_if(ok && need_l, ptr - 1, 0u) >= T.t ? 1u : 0u;
-        e |= ldg_u8_if(ok && need_r, ptr + 32, 0u) >= T.t ? 0x80000000u : 0u;
-        eb[slot] = e;
+        ebl[slot] = ldg_u8_if(ok && need_l, ptr - 1, 0u);
+        ebr[slot] = ldg_u8_if(ok && need_r, ptr + 32, 0u);
+    };
+    auto edge_bits = [&](int slot) -> uint32_t {
+        return (ebl[slot] >= (uint32_t)T.t ? 1u : 0u) | (ebr[slot] >= (uint32_t)T.t ? 0x80000000u : 0u);
     };
     auto word = [&](int slot) -> uint32_t {
         return (okm >> slot) & 1u ? pack32_any(ra[slot], rb2[slot], T) : 0xFFFFFFFFu;
@@ -728,7 +739,7 @@ edge_roll_u8_kernel(const RegParams p) {
     for (int i = 0; i < Q; ++i) issue(i, i);
     uint32_t w_up = word(0);
     uint32_t w_c = word(1);
-    uint32_t e_c = eb[1];
+    uint32_t e_c = edge_bits(1);
     for (int r0 = 0; r0 < RSL; r0 += Q) {
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
@@ -753,7 +764,7 @@ edge_roll_u8_kernel(const RegParams p) {
             }
             w_up = w_c;
             w_c = w_d;
-            e_c = eb[sd];
+            e_c = edge_bits(sd);
             o += p.out_stride;
             if (++y == p.h) y = 0;
         }

@@ -49,6 +49,20 @@ def test_u8_midsize_default_dispatch(cuda_dev, h, w):
     assert (got32 == cscan.scan_u8(a, 1)).all()
 
 
+def test_u8_rolling_strips_rows_straddling_warps(cuda_dev):
+    """K2r (32-row rolling strips; needs >= 303 104 threads) on 640-px rows: 20 words
+    per row, so warps straddle rows and lanes 0 / 31 fetch their neighbour bytes."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(11)
+    a = (rng.random((1100, 480, 640)) < 0.7).astype(np.uint8)
+    got = cu.pack_edges_u8(torch.from_numpy(a).to(cuda_dev), 1).cpu().numpy().view(np.uint32)
+    exp = cscan.scan_u8(a, 1)
+    assert (got == exp).all(), np.argwhere(got != exp)[:4]
+
+
 @pytest.mark.parametrize("h,w,bits", [(8192, 8000, 32), (8192, 8000, 64), (3001, 10016, 32),
                                       (5000, 4100, 64), (2, 8000, 32), (3, 1056, 64)])
 def test_packed_ragged_flat(cuda_dev, h, w, bits):
