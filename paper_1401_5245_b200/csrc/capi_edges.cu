@@ -195,10 +195,13 @@ constexpr int64_t kTma2MinSegs = 12000;
 // one-shot K2, whose warps straddle rows that are not 1024-px multiples (batches of
 // 1920x1080 frames: 35.6 -> 21.7 us, 0.64 -> 1.05 of the copy peak; 1600x1200: 21.0 ->
 // 14.2 us; 1280x1024: 16.1 -> 14.4 us; 1024-px rows stay with K2: 12.8 vs 19.7 us).
-// BITEDGE_TMA2_MINW overrides it.
-inline int64_t tma2_min_width() {
+// Rows that are not 32-byte multiples (K2 then loads 128 bits at a time, or word by
+// word) move over from 1040 px: batches of 1200-px rows 89.8 -> 58.5 us (0.44 -> 0.68),
+// 1250-px rows 40.4 -> 22.8 us, 1100-px rows 19.7 -> 16.7 us; 32-byte rows of 1056 px
+// are faster in K2 (15.1 vs 20.1 us).  BITEDGE_TMA2_MINW overrides both.
+inline int64_t tma2_min_width(bool rows32) {
     if (const char *v = knob(KN_TMA2_MINW)) return atoll(v);
-    return 1280;
+    return rows32 ? 1280 : 1040;
 }
 
 // K2t2 strip height for the 0/1 pack, from the launch's row segments T = rows x
@@ -281,7 +284,7 @@ int try_reg_u8_unal(const void *in, int64_t in_row_bytes, uint32_t *o_edges, uin
     // rows >= 2048 px: the TMA ring (K2t2) with granule-aligned copies and a
     // per-row realignment of the packed words (16384 x 16100: 45 -> 95 % of the
     // copy peak); K2 UNAL below otherwise
-    if (G.w >= tma2_min_width() && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
+    if (G.w >= tma2_min_width(false) && !knob(KN_NO_TMA) && !knob(KN_NO_TMA_UNAL)) {
         const int64_t nseg = (G.w + 2047) / 2048;
         const int64_t nwarps32 = (row_hi - row_lo + 31) / 32 * nseg;
         // (no minimum work from 2048 px, unlike aligned rows: at 4096 x 4100 the ring is
@@ -620,7 +623,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     }
     const int64_t rows = row_hi - row_lo;
     // uint8 rows >= 1024 px with enough work: per-warp TMA ring (K2t)
-    const int64_t tma2_minw = tma2_min_width();
+    const int64_t tma2_minw = tma2_min_width(rp.v8 != 0);
     if (input_kind == 1 && (G.w >= tma2_minw || (u64_out && !u64_k2)) && !knob(KN_NO_TMA) &&
         (!knob(KN_TMA1) || u64_out)) {
         const int64_t nseg = (G.w + 2047) / 2048;
@@ -659,8 +662,14 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         const int64_t nseg = (G.w + 1023) / 1024;
         const int64_t nstrips = (rows_total(row_lo, row_hi) + kRSLT - 1) / kRSLT;
         const int64_t nwarps = nstrips * nseg;
+        // Opt-in since K2 / K2r stopped stalling on their neighbour bytes (BITEDGE_TMA1
+        // with enough work, or BITEDGE_FORCE_TMA at any size -- the variant tests): large
+        // batches of 1024-px rows run K2r at 0.89 of the copy peak against K2t's 0.78, and
+        // rows just over 1024 px half-fill K2t's second segment (128 x 1024 x 1152: 61.7
+        // against K2's 32.5 us)
         const bool force = knob(KN_FORCE_TMA) != nullptr;   // tests: any size
-        if ((force || nwarps >= (int64_t)sm_count() * 32) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
+        const bool opt_in = knob(KN_TMA1) && nwarps >= (int64_t)sm_count() * 32;
+        if ((force || opt_in) && (nwarps + 7) / 8 <= 0x7FFFFFFFLL) {
             const unsigned grid = (unsigned)((nwarps + 7) / 8);
             const size_t smem = (size_t)8 * kD * 1056 + (size_t)8 * kD * 8;
             const bool halo = above || below;

@@ -29,7 +29,9 @@ def _pages(h, w, seed):
                                  (12960, 1920),     # 12 frames of 1920 x 1080: one 94 %-full segment
                                  (12000, 1600),     # 78 %-full segments
                                  (12960, 1900),     # ragged 1900-px rows: UNAL ring under 2048 px
-                                 (16000, 1290)])    # 63 %-full ragged segments
+                                 (16000, 1290),     # 63 %-full ragged segments
+                                 (14400, 1200),     # 16-byte rows under 1280 px: the ring from 1040 px
+                                 (13000, 1100)])    # ragged rows under 1280 px
 def test_u8_midsize_default_dispatch(cuda_dev, h, w):
     import torch
 
