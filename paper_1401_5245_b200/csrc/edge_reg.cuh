@@ -502,7 +502,7 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
 // K2 one-shot strips.  UNAL: rows start at any byte (row lengths that are not
 // 16-byte multiples, strided views): a word's 32 bytes come from the 9 aligned
 // 32-bit words around them (L1-cached loads) and one byte permute per word;
-// never read past `in_end`.  Output words go to column c ^ oswap (1: the
+// never read past the aligned 4 (8: 64-bit loads) bytes holding the buffer's last byte.  Output words go to column c ^ oswap (1: the
 // drop-in's uint64 layout; the u64 row's last u32 word may be pure padding).
 // Aligned 4-row strips at 64 registers (4 CTAs/SM; ~20 bytes of spills): a 4096^2
 // raster's 512 CTAs are one wave instead of 1.15 of the 74-register build's 444
@@ -539,6 +539,7 @@ edge_reg_u8_kernel(const RegParams p) {
     uint32_t lbit[RS], rbit[RS];
     {
         uint4 ra[RS + 2], rb2[RS + 2];
+        uint32_t usem = 0u;                            // UNAL: bit i = staged row i was loaded
 #pragma unroll
         for (int i = 0; i < RS + 2; ++i) {
             const char *ptr = base + i * rb;
@@ -549,7 +550,35 @@ edge_reg_u8_kernel(const RegParams p) {
             }
             ra[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
             rb2[i] = ra[i];
-            if (ok && inrow) {
+            if constexpr (UNAL == 1) {
+                // Branch-free, so the loads of all RS + 2 rows are issued before the first
+                // use (with a branch per row -- row present? buffer end? -- every row's
+                // loads waited for the previous row's: 1024 x 256 x 250 26.9 -> 24.3 us,
+                // 64 x 256 x 250 2.43 -> 1.98 us).  A row that does not exist reads the
+                // buffer's first bytes and is whitened after the pack; words past the
+                // buffer's last byte (the last row's last item: padding positions) read
+                // the buffer's last word instead.  (The same change to the 8- / 4-byte
+                // aligned variants cost registers -- 77 / 100 -- and 10 % on large
+                // batches: 256 x 500 x 1000 30.1 -> 33.3 us; they keep their branches.)
+                const bool use = ok && inrow;
+                usem |= use ? (1u << i) : 0u;
+                const char *src = use ? ptr : p.in;
+                // any byte: the 9 aligned words around the 32 bytes + one permute each
+                const uintptr_t pa = (uintptr_t)src;
+                const char *a4 = reinterpret_cast<const char *>(pa & ~(uintptr_t)3);
+                const char *lastw = reinterpret_cast<const char *>(((uintptr_t)p.in_end - 1) & ~(uintptr_t)3);
+                const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(pa & 3);
+                uint32_t tw[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    const char *a = a4 + 4 * k;
+                    tw[k] = __ldg(reinterpret_cast<const uint32_t *>(a < lastw ? a : lastw));
+                }
+                ra[i] = make_uint4(__byte_perm(tw[0], tw[1], sel), __byte_perm(tw[1], tw[2], sel),
+                                   __byte_perm(tw[2], tw[3], sel), __byte_perm(tw[3], tw[4], sel));
+                rb2[i] = make_uint4(__byte_perm(tw[4], tw[5], sel), __byte_perm(tw[5], tw[6], sel),
+                                    __byte_perm(tw[6], tw[7], sel), __byte_perm(tw[7], tw[8], sel));
+            } else if (ok && inrow) {
                 if constexpr (UNAL == 8 || UNAL == 4) {
                     // rows 8- / 4-byte aligned: the 32 bytes as 4 x 64-bit / 8 x 32-bit
                     // loads (a row's last word may read into the next row, never past
@@ -583,29 +612,6 @@ edge_reg_u8_kernel(const RegParams p) {
                     }
                     ra[i] = make_uint4(tw[0], tw[1], tw[2], tw[3]);
                     rb2[i] = make_uint4(tw[4], tw[5], tw[6], tw[7]);
-                } else if constexpr (UNAL == 1) {
-                    const uintptr_t pa = (uintptr_t)ptr;
-                    const uint32_t *a4 = reinterpret_cast<const uint32_t *>(pa & ~(uintptr_t)3);
-                    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(pa & 3);
-                    uint32_t tw[9];
-                    if ((const char *)(a4 + 9) <= p.in_end) {
-#pragma unroll
-                        for (int k = 0; k < 9; ++k) tw[k] = __ldg(a4 + k);
-                    } else {                                   // the buffer's last bytes
-                        const char *b = reinterpret_cast<const char *>(a4);
-#pragma unroll
-                        for (int k = 0; k < 9; ++k) {
-                            uint32_t v = 0u;
-                            for (int j = 0; j < 4; ++j)
-                                if (b + 4 * k + j < p.in_end)
-                                    v |= (uint32_t)(uint8_t)__ldg(b + 4 * k + j) << (8 * j);
-                            tw[k] = v;
-                        }
-                    }
-                    ra[i] = make_uint4(__byte_perm(tw[0], tw[1], sel), __byte_perm(tw[1], tw[2], sel),
-                                       __byte_perm(tw[2], tw[3], sel), __byte_perm(tw[3], tw[4], sel));
-                    rb2[i] = make_uint4(__byte_perm(tw[4], tw[5], sel), __byte_perm(tw[5], tw[6], sel),
-                                        __byte_perm(tw[6], tw[7], sel), __byte_perm(tw[7], tw[8], sel));
                 } else if (V8) {
                     ldg_stream_v8(ptr, ra[i], rb2[i]);
                 } else {
@@ -630,7 +636,10 @@ edge_reg_u8_kernel(const RegParams p) {
             rbit[r] = rbit[r] == 0xFFFFFFFFu ? 0u : (rbit[r] >= (uint32_t)T.t ? 0x80000000u : 0u);
         }
 #pragma unroll
-        for (int i = 0; i < RS + 2; ++i) wd[i] = pack32_any(ra[i], rb2[i], T);
+        for (int i = 0; i < RS + 2; ++i) {
+            wd[i] = pack32_any(ra[i], rb2[i], T);
+            if (UNAL == 1 && !((usem >> i) & 1u)) wd[i] = 0xFFFFFFFFu;
+        }
     }
 
     uint32_t keep = 0xFFFFFFFFu, fixb = 0u, force = 0u;
