@@ -204,6 +204,12 @@ inline int64_t tma2_min_width(bool rows32) {
     return rows32 ? 1280 : 1040;
 }
 
+// K2r (32-row rolling strips) from this many threads (BITEDGE_ROLL_MIN overrides)
+inline int64_t roll_min_threads() {
+    if (const char *v = knob(KN_ROLL_MIN)) return atoll(v);
+    return (int64_t)sm_count() * 2048;
+}
+
 // K2t2 strip height for the 0/1 pack, from the launch's row segments T = rows x
 // 2048-px segments (= warps x strip height).  Many waves of resident warps (24 per
 // SM): 8 rows, the tail is short.  A few waves: the rows are cut into strips that
@@ -695,7 +701,7 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
     // uint8 with 32-byte rows and enough strips to fill the GPU: long rolling strips
     constexpr int kRSL = 32, kQ = 4;
     if (input_kind == 1 && rp.v8 && !u64_out && !o_packed && !knob(KN_NO_ROLL) &&
-        (rows + kRSL - 1) / kRSL * rp.items >= (int64_t)sm_count() * 2048) {
+        (rows + kRSL - 1) / kRSL * rp.items >= roll_min_threads()) {
         rp.nstrips = (rows + kRSL - 1) / kRSL;
         const int64_t g = (rp.nstrips * rp.items + kThreads - 1) / kThreads;
         if (g <= 0x7FFFFFFFLL) {

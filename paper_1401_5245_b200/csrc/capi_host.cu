@@ -23,7 +23,7 @@ const char *const kKnobNames[KN_COUNT] = {
     "BITEDGE_NO_WARPIMG", "BITEDGE_WARPIMG_G4", "BITEDGE_PDL_LATE", "BITEDGE_TMA1",
     "BITEDGE_FORCE_TMA", "BITEDGE_U64_TMA", "BITEDGE_TMA2_RSL8", "BITEDGE_TMA2_RSL32",
     "BITEDGE_NO_ROLL", "BITEDGE_RS", "BITEDGE_PRS", "BITEDGE_UNAL_RS4", "BITEDGE_P4_UNFUSED",
-    "BITEDGE_P4_BYTES", "BITEDGE_PDL", "BITEDGE_NO_FLAT", "BITEDGE_K2P", "BITEDGE_SYNC_BLOCK", "BITEDGE_NO_H16", "BITEDGE_RING", "BITEDGE_NO_TMA_UNAL", "BITEDGE_P4_NO_FLAT", "BITEDGE_P4_FLAT16", "BITEDGE_P4_FLAT_MAX", "BITEDGE_P4_FLAT32", "BITEDGE_TMA2_MIN", "BITEDGE_TMA2_RSL", "BITEDGE_TMA2_MINW"};
+    "BITEDGE_P4_BYTES", "BITEDGE_PDL", "BITEDGE_NO_FLAT", "BITEDGE_K2P", "BITEDGE_SYNC_BLOCK", "BITEDGE_NO_H16", "BITEDGE_RING", "BITEDGE_NO_TMA_UNAL", "BITEDGE_P4_NO_FLAT", "BITEDGE_P4_FLAT16", "BITEDGE_P4_FLAT_MAX", "BITEDGE_P4_FLAT32", "BITEDGE_TMA2_MIN", "BITEDGE_TMA2_RSL", "BITEDGE_TMA2_MINW", "BITEDGE_ROLL_MIN"};
 }  // namespace capi
 }  // namespace bitedge
 

@@ -62,6 +62,7 @@ enum Knob : int {
     KN_TMA2_MIN,
     KN_TMA2_RSL,
     KN_TMA2_MINW,
+    KN_ROLL_MIN,
     KN_COUNT
 };
 extern const char *const kKnobNames[KN_COUNT];
