@@ -15,6 +15,8 @@ done
 timeout -k 10 300 python scripts/k1_widths.py > gpurun_out/fin/k1w.log 2>&1
 timeout -k 10 300 python scripts/u8_widths.py > gpurun_out/fin/u8w.log 2>&1
 timeout -k 10 300 python scripts/u8_mid_sweep.py final > gpurun_out/fin/u8mid.log 2>&1
+timeout -k 10 300 python scripts/u8_batch_sweep.py > gpurun_out/fin/u8batch.log 2>&1
+U8B_SHAPES=256x1024x1024,200x960x1216,128x1024x1152,200x960x1200,64x1000x1250,48x1024x1280,40x1200x1600,64x1080x1900,1100x480x640,1024x200x300,256x500x1000 timeout -k 10 300 python scripts/u8_batch_sweep.py > gpurun_out/fin/u8batch2.log 2>&1
 K1W_SHAPES=6000x6016,10000x10016,12000x11968,12288x12288,16384x16000,16384x16384,24576x24576 timeout -k 10 300 python scripts/k1_widths.py > gpurun_out/fin/k1mid.log 2>&1
 timeout -k 10 300 python scripts/p4_flat_bench.py gpurun_out/fin/p4_flat.txt > gpurun_out/fin/p4_flat.log 2>&1
 timeout -k 10 300 python scripts/p4_ragged_bench.py > gpurun_out/fin/p4_ragged.log 2>&1
