@@ -751,7 +751,10 @@ def e2e_host(args, cfg, base, kind, w, h, lo, hi, dev, world, shard, px_job):
     # step i is submitted before step i-depth+1's result is awaited and read on
     # the host, so each step's sync latency hides behind the next steps' copies
     pend = [None] * depth
-    nwin = 5 if e2e_steps >= 10 else 1
+    # five windows (median) when each still moves >= 1 GB; fewer bytes per window would
+    # time the pipeline's fill and drain, not its rate (C3 at the driver's 20 steps: 4
+    # steps of 8 MB per window read 62-75 % of the plain copies' rate)
+    nwin = 5 if e2e_steps >= 10 and (e2e_steps // 5) * pipe.h2d_bytes >= 1e9 else 1
     per_win = e2e_steps // nwin
     e2e_steps = per_win * nwin
     wms = []
