@@ -191,6 +191,12 @@ int launch_reg_halo(RegParams &rp, int input_kind, int swap, int cw, int rs, uns
 inline int64_t rows_total(int64_t lo, int64_t hi) { return hi - lo; }
 // aligned uint8 rasters take K2t2 from this many row segments (rows x 2048-px segments)
 constexpr int64_t kTma2MinSegs = 12000;
+// thresholded pack (ALU-heavier: halo rows cost more, so longer strips): K2t2 from 24 000
+// row segments with 12-row strips until 32-row strips make 24 warps per SM (8192^2, t = 128:
+// 16.9 -> 12.3 us, 0.68 -> 0.94 of the copy peak; 12288^2 37.6 -> 27.1 us; a batch of 64
+// 1920x1080 frames 33.5 -> 25.4 us; 5000x5008 stays with K2: 7.1 us against 8.6)
+constexpr int kThrMidRows = 12;
+constexpr int64_t kTma2MinSegsThr = 24000;
 // ... and from this row width: a 2048-px segment that is >= 62 % full still beats the
 // one-shot K2, whose warps straddle rows that are not 1024-px multiples (batches of
 // 1920x1080 frames: 35.6 -> 21.7 us, 0.64 -> 1.05 of the copy peak; 1600x1200: 21.0 ->
@@ -649,12 +655,21 @@ int try_reg(const void *in, int input_kind, int64_t in_row_bytes, const void *ab
         if (const char *v = knob(KN_TMA2_MIN)) min_segs = atoll(v);
         // (rows under 2048 px -- uint64 words from 1024 px -- half-fill their segments:
         // 16x1024^2 is 6.8 us here against K2's 3.6)
-        const bool enough = (short_strips && G.w >= tma2_minw)
-                                ? rows_total(row_lo, row_hi) * nseg >= min_segs
-                                : nwarps32 >= (int64_t)sm_count() * 24;
+        const bool big32 = nwarps32 >= (int64_t)sm_count() * 24;
+        if (!short_strips && !knob(KN_TMA2_MIN)) min_segs = kTma2MinSegsThr;
+        const bool enough = G.w >= tma2_minw ? rows_total(row_lo, row_hi) * nseg >= min_segs
+                                             : big32;
         if ((force || enough) && (nwarps32 * 4 + 7) / 8 <= 0x7FFFFFFFLL) {
             const bool halo = above || below;
-            if (!short_strips) return launch_tma2<32>(rp, multi, halo, nseg, st);
+            if (!short_strips) {
+                // thresholded pack: 32-row strips for many waves; fewer warps than that
+                // take BITEDGE_TMA2_RSL / kThrMidRows-row strips at run time
+                const char *rv = knob(KN_TMA2_RSL);
+                if (big32 && !rv) return launch_tma2<32>(rp, multi, halo, nseg, st);
+                rp.rsl = rv ? atoi(rv) : kThrMidRows;
+                if (rp.rsl < 2 || rp.rsl > 4096) rp.rsl = kThrMidRows;
+                return launch_tma2<0>(rp, multi, halo, nseg, st);
+            }
             rp.rsl = tma2_strip_rows(rows_total(row_lo, row_hi), nseg, G.w >= tma2_minw);
             return rp.rsl == 8 ? launch_tma2<8>(rp, multi, halo, nseg, st)
                                : launch_tma2<0>(rp, multi, halo, nseg, st);

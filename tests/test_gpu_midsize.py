@@ -51,6 +51,26 @@ def test_u8_midsize_default_dispatch(cuda_dev, h, w):
     assert (got32 == cscan.scan_u8(a, 1)).all()
 
 
+@pytest.mark.parametrize("h,w,t", [(8192, 4096, 128), (13000, 1920, 77), (6200, 8192, 200)])
+def test_threshold_midsize_default_dispatch(cuda_dev, h, w, t):
+    """F2 (threshold fused into the pack, reference SPEC.md:237-245) on rasters that
+    take K2t2's 12-row run-time strips: white iff sample >= t."""
+    import torch
+
+    from paper_1401_5245_b200 import cuda as cu
+
+    rng = np.random.default_rng(h + w + t)
+    g = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    g[:: max(1, h // 9)] = 0
+    g[:, :: max(1, w // 7)] = 255
+    x = torch.from_numpy(g).to(cuda_dev)
+    binary = (g >= t).astype(np.uint8)
+    for fill in (1, 0):
+        got = cu.threshold_edges_u8(x, t, fill).cpu().numpy().view(np.uint32)
+        exp = cscan.scan_u8(binary, fill)
+        assert (got == exp).all(), (h, w, t, fill, np.argwhere(got != exp)[:4])
+
+
 def test_u8_rolling_strips_rows_straddling_warps(cuda_dev):
     """K2r (32-row rolling strips; needs >= 303 104 threads) on 640-px rows: 20 words
     per row, so warps straddle rows and lanes 0 / 31 fetch their neighbour bytes."""
