@@ -502,8 +502,9 @@ edge_warp_img_kernel(const RegParams p, int G, int64_t nimg) {
 // K2 one-shot strips.  UNAL: rows start at any byte (row lengths that are not
 // 16-byte multiples, strided views): a word's 32 bytes come from the 9 aligned
 // 32-bit words around them (L1-cached loads) and one byte permute per word;
-// never read past the aligned 4 (8: 64-bit loads) bytes holding the buffer's last byte.  Output words go to column c ^ oswap (1: the
-// drop-in's uint64 layout; the u64 row's last u32 word may be pure padding).
+// never read past the aligned 4 (8: 64-bit loads) bytes holding the buffer's last
+// byte.  Output words go to column c ^ oswap (1: the drop-in's uint64 layout; the
+// u64 row's last u32 word may be pure padding).
 // Aligned 4-row strips at 64 registers (4 CTAs/SM; ~20 bytes of spills): a 4096^2
 // raster's 512 CTAs are one wave instead of 1.15 of the 74-register build's 444
 // (4.58 -> 4.36 us, 8.25 -> 6.38 us on one stream; 16x1024^2 6.31 -> 5.52 us).  The
