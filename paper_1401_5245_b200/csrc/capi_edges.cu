@@ -197,17 +197,18 @@ constexpr int64_t kTma2MinSegs = 12000;
 // 1920x1080 frames 33.5 -> 25.4 us; 5000x5008 stays with K2: 7.1 us against 8.6)
 constexpr int kThrMidRows = 12;
 constexpr int64_t kTma2MinSegsThr = 24000;
-// ... and from this row width: a 2048-px segment that is >= 62 % full still beats the
-// one-shot K2, whose warps straddle rows that are not 1024-px multiples (batches of
-// 1920x1080 frames: 35.6 -> 21.7 us, 0.64 -> 1.05 of the copy peak; 1600x1200: 21.0 ->
-// 14.2 us; 1280x1024: 16.1 -> 14.4 us; 1024-px rows stay with K2: 12.8 vs 19.7 us).
+// ... and from this row width: a 2048-px segment that is >= 69 % full beats the one-shot
+// K2 (batches of 1920x1080 frames: 35.6 -> 21.7 us, 0.64 -> 1.05 of the copy peak;
+// 1600x1200: 16.7 -> 14.1 us).  K2 runs 32-byte rows of 768 .. 1536 px at a flat 0.79
+// since its neighbour-byte fix and K2t2 at about its segment fill, so they cross at
+// ~1400 px (1344: 14.4 us both; 1408: 15.0 vs 14.5; 1280: 13.6 vs 14.5).
 // Rows that are not 32-byte multiples (K2 then loads 128 bits at a time, or word by
 // word) move over from 1040 px: batches of 1200-px rows 89.8 -> 58.5 us (0.44 -> 0.68),
 // 1250-px rows 40.4 -> 22.8 us, 1100-px rows 19.7 -> 16.7 us; 32-byte rows of 1056 px
 // are faster in K2 (15.1 vs 20.1 us).  BITEDGE_TMA2_MINW overrides both.
 inline int64_t tma2_min_width(bool rows32) {
     if (const char *v = knob(KN_TMA2_MINW)) return atoll(v);
-    return rows32 ? 1280 : 1040;
+    return rows32 ? 1408 : 1040;
 }
 
 // K2r (32-row rolling strips) from this many threads (BITEDGE_ROLL_MIN overrides)

@@ -28,6 +28,7 @@ def _pages(h, w, seed):
                                  (7000, 6148),      # ragged rows through the UNAL ring
                                  (12960, 1920),     # 12 frames of 1920 x 1080: one 94 %-full segment
                                  (12000, 1600),     # 78 %-full segments
+                                 (12288, 1408),     # the narrowest 32-byte rows the ring takes
                                  (12960, 1900),     # ragged 1900-px rows: UNAL ring under 2048 px
                                  (16000, 1290),     # 63 %-full ragged segments
                                  (14400, 1200),     # 16-byte rows under 1280 px: the ring from 1040 px
