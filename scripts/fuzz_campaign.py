@@ -1,7 +1,8 @@
 """Time-bounded random parity campaign on the GPU (default dispatch, no knobs):
 uint8 batches, packed u32 / u64 rasters and P4 payloads of random shapes --
 many of them large enough to reach the flat kernels (K1f, K1p), the TMA ring's
-run-time strips and the UNAL variants -- against the C scanner.
+run-time strips and the UNAL variants -- and thresholded grayscale batches,
+against the C scanner.
 Usage: fuzz_campaign.py [seconds] [seed]"""
 import os
 import sys
@@ -58,6 +59,12 @@ while time.time() - t0 < budget:
         view.copy_(x)
         got = cu.pack_edges_u8(view, fill).cpu().numpy().view(np.uint32)
         assert (got == exp).all(), ("u8 strided", tag, pad, off)
+    # thresholded pack (F2): white iff sample >= t
+    if n * h * w < 60_000_000:
+        t = int(rng.choice([0, 1, 2, 77, 128, 200, 255]))
+        g = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+        got = cu.threshold_edges_u8(torch.from_numpy(g).to(dev), t, fill).cpu().numpy().view(np.uint32)
+        assert (got == cscan.scan_u8((g >= t).astype(np.uint8), fill)).all(), ("thr", tag, t)
     # packed u32 and u64 words
     pk = torch.from_numpy(P.pack_u32(a).view(np.int32)).to(dev)
     got = cu.edges_packed(pk, w, fill).cpu().numpy().view(np.uint32)
